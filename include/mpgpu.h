@@ -1,0 +1,164 @@
+/* mpgpu.h -- C-ABI of the B200-native multiple-precision GEMM / LU library
+ * (libmpgpu.so, built from paper_1410_1599_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference's MP matmul / LU hot path
+ * (/root/reference/proj/include/mpmm).  Every entry point below names the
+ * reference interface it replaces; the C++ shim in include/mpmm_gpu.hpp binds the
+ * reference's own signatures to it.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host buffers are caller-owned; device
+ *     matrices are owned by the handle that allocated them.
+ *   - Host MP arrays are structure-of-arrays ("SoA"): for N = rows*cols elements
+ *     in row-major order and a host limb count Lh >= ceil(prec/32):
+ *        limbs[k*N + e]  32-bit limb k of element e, k = Lh-1 most significant;
+ *                        the MSB of limb Lh-1 is set for nonzero values and bits
+ *                        below prec are zero (MPFR's mantissa, regrouped in 32-bit
+ *                        limbs);
+ *        exp[e]          MPFR exponent (value = (-1)^sign * 0.m * 2^exp with
+ *                        0.m in [1/2, 1)), or MPGPU_EXP_ZERO for a zero;
+ *        sign[e]         1 for negative (zeros keep their sign, as in MPFR).
+ *     NaN / Inf are not representable: callers reject them (DomainError).
+ *   - Rounding is MPFR_RNDN (precision.hpp:22) after every multiply and every
+ *     add, exactly as the reference; results are bit-identical to the reference
+ *     wherever the reference's operation order is replayed (all of them: Simple,
+ *     Block, Strassen, Winograd, pivot-free blocked LU).
+ *   - Return codes map 1:1 onto the reference's exception types (errors.hpp:10-48).
+ *   - Calls on one handle are serialised (internal mutex) and synchronous.
+ */
+#ifndef MPGPU_H
+#define MPGPU_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPGPU_OK 0
+#define MPGPU_ERR_DIMENSION 1 /* mpmm::DimensionError  (errors.hpp:15-17) */
+#define MPGPU_ERR_DOMAIN 2    /* mpmm::DomainError     (errors.hpp:21-23) */
+#define MPGPU_ERR_SINGULAR 3  /* mpmm::SingularError   (errors.hpp:26-31), pivot index out-param */
+#define MPGPU_ERR_CUDA 4      /* device / runtime failure (no reference analogue) */
+#define MPGPU_ERR_NOMEM 5     /* device allocation failed */
+
+#define MPGPU_EXP_ZERO INT32_MIN
+#define MPGPU_MAX_PREC 1024 /* largest precision with a device kernel (32 limbs) */
+
+/* mpmm::Algorithm (fastmm.hpp:13) */
+enum { MPGPU_SIMPLE = 0, MPGPU_BLOCK = 1, MPGPU_STRASSEN = 2, MPGPU_WINOGRAD = 3 };
+
+typedef struct mpgpu_handle mpgpu_handle;
+
+/* Device matrix: row-major AoS records of mpgpu_record_words(nlimbs) 32-bit words
+ * (limbs[0..nlimbs-1], exp, sign, padding) -- opaque to callers except for the
+ * pointer, which may be handed to NCCL / torch for raw transfers. */
+typedef struct {
+  int64_t rows, cols;
+  int32_t prec;   /* bits (mpmm::PrecisionContext, precision.hpp:18-36) */
+  int32_t nlimbs; /* device limbs per element */
+  uint32_t* rec;  /* device pointer */
+  int64_t ld;     /* elements between consecutive rows */
+  int32_t owned;  /* 1 if allocated by mpgpu_alloc_matrix */
+} mpgpu_mat;
+
+/* Per-call statistics.  mul / addsub are the reference's OpCounter tallies
+ * (opcounter.hpp:9-20) for the same call, equal to count_fast / count_simple. */
+typedef struct {
+  uint64_t mul, addsub;
+  uint64_t leaf_madds; /* MP multiply-adds executed by the leaf GEMM kernel(s) */
+  double device_ms;    /* CUDA-event time of the device work of the call */
+  double leaf_ms;      /* CUDA-event time of the leaf GEMM launch(es) */
+  double preadd_ms, postadd_ms;
+  int32_t launches; /* kernels launched by the call */
+  int32_t depth;    /* Strassen / Winograd recursion depth used */
+} mpgpu_stats;
+
+/* ---- handle ------------------------------------------------------------ */
+int mpgpu_init(int device, mpgpu_handle** out);
+void mpgpu_destroy(mpgpu_handle* h);
+const char* mpgpu_last_error(const mpgpu_handle* h);
+/* run subsequent work on an external cudaStream_t (NULL: the handle's own stream) */
+int mpgpu_set_stream(mpgpu_handle* h, void* cuda_stream);
+void* mpgpu_get_stream(mpgpu_handle* h);
+int mpgpu_synchronize(mpgpu_handle* h);
+
+/* device limb count used for a precision (0 if prec is outside [2, MPGPU_MAX_PREC]) */
+int mpgpu_nlimbs_for(int32_t prec);
+int mpgpu_record_words(int32_t nlimbs);
+
+/* ---- matrices (mpmm::Matrix, matrix.hpp:20-42) --------------------------- */
+int mpgpu_alloc_matrix(mpgpu_handle* h, int64_t rows, int64_t cols, int32_t prec, mpgpu_mat* out);
+int mpgpu_free_matrix(mpgpu_handle* h, mpgpu_mat* m);
+/* host SoA (host_nlimbs limbs per element) <-> device records */
+int mpgpu_upload(mpgpu_handle* h, mpgpu_mat* m, const uint32_t* limbs, const int32_t* exp,
+                 const uint8_t* sign, int32_t host_nlimbs);
+int mpgpu_download(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                   int32_t host_nlimbs);
+
+/* ---- GEMM --------------------------------------------------------------
+ * C = A * B at C->prec, replacing
+ *   algo SIMPLE   : simple_mul(A, B, ctx[, ops])            matrix.hpp:178-184
+ *   algo BLOCK    : block_mul(A, B, param=n_min, ctx[, ops]) matrix.hpp:225-233
+ *   algo STRASSEN / WINOGRAD :
+ *                   fast_mul(A, B, {algo, param=n_min}, ctx) fastmm.hpp:244-255
+ * Checks in the reference's order: inner dimension (DIMENSION), param == 0 for
+ * BLOCK / fast (DIMENSION), unknown algo (DOMAIN); A, B and C must share one
+ * precision on the device path (DOMAIN otherwise -- documented deviation).
+ * stats may be NULL. */
+int mpgpu_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B,
+               mpgpu_mat* C, mpgpu_stats* stats);
+
+/* Same, from and to HOST SoA buffers (the reference-facing call: upload, multiply,
+ * download).  C buffers must hold m*n elements of host_nlimbs limbs. */
+int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int64_t m, int64_t l,
+                    int64_t n, const uint32_t* a_limbs, const int32_t* a_exp, const uint8_t* a_sign,
+                    const uint32_t* b_limbs, const int32_t* b_exp, const uint8_t* b_sign,
+                    uint32_t* c_limbs, int32_t* c_exp, uint8_t* c_sign, int32_t host_nlimbs,
+                    mpgpu_stats* stats);
+
+/* fast_mul with the reference's TopTrace (fastmm.hpp:47-51): writes the top-level
+ * intermediates as device matrices packed back to back into trace_rec (sums
+ * S1..S8 for Winograd -- 4 of hm x hl then 4 of hl x hn --, products P1..P7 / M1..M7
+ * (hm x hn), and T1, T2 (hm x hn) for Winograd); counts[3] = {sums, products, t}. */
+int mpgpu_fast_mul_trace(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A,
+                         const mpgpu_mat* B, mpgpu_mat* C, uint32_t* trace_rec, int* counts);
+
+/* elementwise add / sub (matrix.hpp:166-175): C = A +- B */
+int mpgpu_addsub(mpgpu_handle* h, int is_sub, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C);
+/* elementwise scalar op over equal-shaped matrices: 0 add, 1 sub, 2 mul, 3 div
+ * (precision.hpp:127-161); division by zero -> SINGULAR */
+int mpgpu_vec_op(mpgpu_handle* h, int op, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C);
+
+/* ---- LU ----------------------------------------------------------------
+ * In-place blocked LU of the square matrix A (packed unit-lower L \ U, Doolittle),
+ * replacing lu_blocked(A, {K, kernel, n_min}, ctx, schur_ops) (blocklu.hpp:121-146).
+ * pivoting = 0: the reference's pivot-free algorithm, bit-exact.  pivoting = 1:
+ * partial pivoting over the tall panel (first maximal |a_id|, LAPACK ipiv in
+ * piv_out[n], 0-based) -- an extension the reference lacks.  On a zero pivot
+ * returns SINGULAR with *zero_pivot = 1-based index (blocklu.hpp:46-47).
+ * stats->mul/addsub accumulate the Schur multiply counts (schur_ops). */
+int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min,
+                     int pivoting, int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats);
+/* Ly = Pb, Ux = y (blocklu.hpp:215-245); piv may be NULL (pivot-free factors). */
+int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b,
+                   mpgpu_mat* x, int64_t* zero_pivot);
+
+/* ---- host-side model / plan / inputs ------------------------------------ */
+/* count_fast (opmodel.hpp:30-44); SIMPLE / BLOCK give count_simple */
+int mpgpu_count_fast(int algo, int64_t m, int64_t l, int64_t n, int64_t n_min, uint64_t* out2);
+/* recursion_plan (fastmm.hpp:68-85): rows of 8 int64 {level, m,l,n, pm,pl,pn, base} */
+int mpgpu_recursion_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out, int max_levels,
+                         int* count);
+/* Seeded inputs into host SoA buffers (Prng64, matgen.hpp:13-42):
+ *   kind 0: gen_random (matgen.hpp:45-52), 53-bit dyadic uniform [-1,1) rounded at prec
+ *   kind 1: full-mantissa uniform [-1,1): (k - 2^p) / 2^p, k = top p+1 bits of the
+ *           concatenated top53() draws (exact at prec)
+ *   kind 2: mantissa uniform in [1/2,1) with all prec bits random, exponent uniform
+ *           in [-20, 20], random sign (BASELINE config 3) */
+int mpgpu_gen(int kind, int64_t N, uint64_t seed, int32_t prec, uint32_t* limbs, int32_t* exp,
+              uint8_t* sign, int32_t host_nlimbs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

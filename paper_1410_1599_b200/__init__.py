@@ -1,0 +1,13 @@
+"""paper_1410_1599_b200 -- B200-native multiple-precision Simple / Block /
+Strassen / Winograd matrix multiplication and blocked LU (drop-in for the MPFR
+reference's mpmm hot path).  See DESIGN.md and include/mpgpu.h."""
+from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix, Dims3, DimensionError,
+                   DomainError, Error, FastMMConfig, FastMMResult, LUFactors, Matrix, OpCounter,
+                   PrecisionContext, RecursionLevel, SingularError, Stats, TopTrace, add, algorithm_name,
+                   block_mul, count_fast, count_simple, equal_values, fast_mul, handle, identical,
+                   lu_blocked, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
+                   record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
+                   solve_columnwise, sub, vec_op)
+from .matgen import Prng64, from_ints, gen_random, gen_scaled, gen_uniform_full, to_fractions
+
+__all__ = [n for n in dir() if not n.startswith("_")]

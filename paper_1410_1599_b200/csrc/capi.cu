@@ -1,0 +1,950 @@
+// capi.cu -- the extern "C" boundary (include/mpgpu.h) and the host-side driver:
+// handle / memory management, the breadth-first Strassen / Winograd recursion
+// driver (replacing fastmm.hpp:99-229's depth-first recursion), the op model and
+// the seeded input generators.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/mpgpu.h"
+#include "kernels.h"
+#include "mp_arith.cuh"
+
+struct mpgpu_handle {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  uint32_t* d_err = nullptr;
+  int64_t* d_piv = nullptr;
+  int64_t d_piv_cap = 0;
+  std::mutex mu;
+  std::string last_error;
+};
+
+namespace {
+
+using mpg::rec_stride;
+
+int fail(mpgpu_handle* h, int code, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->last_error = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(h, expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((h), e_ == cudaErrorMemoryAllocation ? MPGPU_ERR_NOMEM : MPGPU_ERR_CUDA, \
+                  "%s: %s", #expr, cudaGetErrorString(e_));                                 \
+  } while (0)
+
+constexpr int kLimbOptions[] = {1, 2, 4, 8, 16, 32};
+
+int nlimbs_for(int32_t prec) {
+  if (prec < 2 || prec > MPGPU_MAX_PREC) return 0;
+  const int need = (prec + 31) / 32;
+  for (int L : kLimbOptions)
+    if (L >= need) return L;
+  return 0;
+}
+
+template <class F>
+int dispatch_L(int L, F&& f) {
+  switch (L) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    default: return MPGPU_ERR_DOMAIN;
+  }
+}
+
+// RAII device scratch on the handle's stream (stream-ordered pool allocator)
+struct DevBuf {
+  mpgpu_handle* h = nullptr;
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  cudaError_t alloc(mpgpu_handle* hh, size_t bytes) {
+    release();
+    h = hh;
+    return cudaMallocAsync(&p, bytes < 16 ? 16 : bytes, h->stream);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, h->stream);
+    p = nullptr;
+  }
+  uint32_t* u32() const { return static_cast<uint32_t*>(p); }
+};
+
+struct Timer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer(bool enabled, cudaStream_t s) : on(enabled), st(s) {
+    if (on) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  // returns elapsed ms (synchronises on the end event)
+  double stop() {
+    if (!on) return 0.0;
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+void count_fast_rec(int algo, int64_t m, int64_t l, int64_t n, int64_t n_min, uint64_t* out) {
+  if (algo < MPGPU_STRASSEN || std::min({m, l, n}) <= n_min) {
+    out[0] = (uint64_t)m * l * n;
+    out[1] = (uint64_t)m * n * (l - 1);
+    return;
+  }
+  const int64_t hm = (m + m % 2) / 2, hl = (l + l % 2) / 2, hn = (n + n % 2) / 2;
+  uint64_t half[2];
+  count_fast_rec(algo, hm, hl, hn, n_min, half);
+  const uint64_t ka = algo == MPGPU_STRASSEN ? 5 : 4, kb = ka, kc = algo == MPGPU_STRASSEN ? 8 : 7;
+  out[0] = 7 * half[0];
+  out[1] = 7 * half[1] + ka * hm * hl + kb * hl * hn + kc * hm * hn;
+}
+
+struct Level {
+  int64_t m, l, n;
+};
+
+// recursion_plan (fastmm.hpp:68-85): dims entering each level; last is the base case
+std::vector<Level> plan_levels(int64_t m, int64_t l, int64_t n, int64_t n_min) {
+  std::vector<Level> v;
+  for (;;) {
+    v.push_back({m, l, n});
+    if (std::min({m, l, n}) <= n_min) return v;
+    m = (m + m % 2) / 2;
+    l = (l + l % 2) / 2;
+    n = (n + n % 2) / 2;
+  }
+}
+
+int check_err(mpgpu_handle* h) {
+  uint32_t e = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&e, h->d_err, sizeof e, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaGetLastError());
+  if (e & mpg::ERR_DIV_ZERO) return fail(h, MPGPU_ERR_SINGULAR, "division by zero");
+  if (e & mpg::ERR_EXP_RANGE)
+    return fail(h, MPGPU_ERR_DOMAIN, "exponent outside MPFR's default range (overflow/underflow)");
+  return MPGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM driver.  Simple / Block: one leaf launch.  Strassen / Winograd: breadth-
+// first over the recursion levels -- per level one fused pre-add launch per operand
+// side over all 7^lev nodes, then ONE batched leaf GEMM over all 7^d leaves, then
+// one fused post-add launch per level back up.  Same operation DAG as the
+// reference's depth-first recursion, so the result is bit-identical.
+// ---------------------------------------------------------------------------
+template <int L>
+int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_t lda, const uint32_t* B,
+             int64_t ldb, uint32_t* C, int64_t ldc, int64_t m, int64_t l, int64_t n, int sh,
+             mpgpu_stats* stats, int sub_from_c) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  const bool timing = stats != nullptr;
+  Timer total(timing, st);
+  int launches = 0;
+  auto leaf = [&](const uint32_t* a, int64_t la, const uint32_t* b, int64_t lb, uint32_t* c, int64_t lc,
+                  int64_t mm, int64_t ll, int64_t nn, int64_t kb, int batch, int subc) {
+    mpg::GemmArgs g{};
+    g.A = a;
+    g.B = b;
+    g.C = c;
+    g.strideA = mm * ll;
+    g.strideB = ll * nn;
+    g.strideC = mm * nn;
+    g.lda = la;
+    g.ldb = lb;
+    g.ldc = lc;
+    g.m = (int)mm;
+    g.l = (int)ll;
+    g.n = (int)nn;
+    g.kb = (int)std::min<int64_t>(kb, ll);
+    g.batch = batch;
+    g.sh = sh;
+    g.err = h->d_err;
+    g.sub_from_c = subc;
+    mpg::launch_gemm<L>(g, st);
+    ++launches;
+  };
+  if (stats) stats->depth = 0;
+  if (algo == MPGPU_SIMPLE || algo == MPGPU_BLOCK) {
+    Timer tl(timing, st);
+    leaf(A, lda, B, ldb, C, ldc, m, l, n, algo == MPGPU_SIMPLE ? l : param, 1, sub_from_c);
+    if (stats) {
+      stats->leaf_ms = tl.stop();
+      stats->leaf_madds = (uint64_t)m * l * n;
+    }
+  } else {
+    const std::vector<Level> lv = plan_levels(m, l, n, param);
+    const int d = (int)lv.size() - 1;
+    if (stats) stats->depth = d;
+    if (d == 0) {
+      Timer tl(timing, st);
+      leaf(A, lda, B, ldb, C, ldc, m, l, n, l, 1, sub_from_c);
+      if (stats) {
+        stats->leaf_ms = tl.stop();
+        stats->leaf_madds = (uint64_t)m * l * n;
+      }
+    } else {
+      // level 0 operands must be dense for the pre-add kernel
+      DevBuf a0, b0;
+      const uint32_t* pa = A;
+      const uint32_t* pb = B;
+      if (lda != l) {
+        CUDA_TRY(h, a0.alloc(h, sizeof(uint32_t) * S * m * l));
+        mpg::launch_copy2d<L>(A, lda, a0.u32(), l, (int)m, (int)l, st);
+        ++launches;
+        pa = a0.u32();
+      }
+      if (ldb != n) {
+        CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * l * n));
+        mpg::launch_copy2d<L>(B, ldb, b0.u32(), n, (int)l, (int)n, st);
+        ++launches;
+        pb = b0.u32();
+      }
+      std::vector<DevBuf> opA(d + 1), opB(d + 1), prod(d + 1);
+      Timer tpre(timing, st);
+      int64_t nodes = 1;
+      for (int lev = 0; lev < d; ++lev) {
+        const Level& P = lv[lev];
+        const Level& Q = lv[lev + 1];
+        const uint32_t* srcA = lev == 0 ? pa : opA[lev].u32();
+        const uint32_t* srcB = lev == 0 ? pb : opB[lev].u32();
+        CUDA_TRY(h, opA[lev + 1].alloc(h, sizeof(uint32_t) * S * nodes * 7 * Q.m * Q.l));
+        CUDA_TRY(h, opB[lev + 1].alloc(h, sizeof(uint32_t) * S * nodes * 7 * Q.l * Q.n));
+        mpg::launch_preadd<L>(algo, 0, srcA, nodes, (int)P.m, (int)P.l, opA[lev + 1].u32(), sh, h->d_err, st);
+        mpg::launch_preadd<L>(algo, 1, srcB, nodes, (int)P.l, (int)P.n, opB[lev + 1].u32(), sh, h->d_err, st);
+        launches += 2;
+        if (lev > 0) {
+          opA[lev].release();
+          opB[lev].release();
+        }
+        nodes *= 7;
+      }
+      a0.release();
+      b0.release();
+      if (stats) stats->preadd_ms = tpre.stop();
+      const Level& D = lv[d];
+      CUDA_TRY(h, prod[d].alloc(h, sizeof(uint32_t) * S * nodes * D.m * D.n));
+      {
+        Timer tl(timing, st);
+        leaf(opA[d].u32(), D.l, opB[d].u32(), D.n, prod[d].u32(), D.n, D.m, D.l, D.n, D.l, (int)nodes, 0);
+        if (stats) {
+          stats->leaf_ms = tl.stop();
+          stats->leaf_madds = (uint64_t)nodes * D.m * D.l * D.n;
+        }
+      }
+      opA[d].release();
+      opB[d].release();
+      Timer tpost(timing, st);
+      DevBuf top;
+      for (int lev = d - 1; lev >= 0; --lev) {
+        nodes /= 7;
+        const Level& P = lv[lev];
+        uint32_t* dst;
+        if (lev == 0 && ldc == n && !sub_from_c) {
+          dst = C;
+        } else if (lev == 0) {
+          CUDA_TRY(h, top.alloc(h, sizeof(uint32_t) * S * m * n));
+          dst = top.u32();
+        } else {
+          CUDA_TRY(h, prod[lev].alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
+          dst = prod[lev].u32();
+        }
+        mpg::launch_postadd<L>(algo, prod[lev + 1].u32(), nodes, (int)P.m, (int)P.n, dst, nullptr, sh,
+                               h->d_err, st);
+        ++launches;
+        prod[lev + 1].release();
+      }
+      if (top.p) {
+        if (sub_from_c) {
+          return fail(h, MPGPU_ERR_DOMAIN, "internal: strided fast Schur epilogue not routed here");
+        }
+        mpg::launch_copy2d<L>(top.u32(), n, C, ldc, (int)m, (int)n, st);
+        ++launches;
+      }
+      if (stats) stats->postadd_ms = tpost.stop();
+    }
+  }
+  if (stats) {
+    stats->device_ms = total.stop();
+    stats->launches = launches;
+  }
+  return MPGPU_OK;
+}
+
+int validate_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B,
+                  const mpgpu_mat* C) {
+  if (!A || !B || !C) return fail(h, MPGPU_ERR_DIMENSION, "null matrix");
+  if (A->cols != B->rows)
+    return fail(h, MPGPU_ERR_DIMENSION, "inner dimension mismatch: %lld vs %lld", (long long)A->cols,
+                (long long)B->rows);
+  if ((algo == MPGPU_BLOCK || algo == MPGPU_STRASSEN || algo == MPGPU_WINOGRAD) && param == 0)
+    return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
+  if (algo < MPGPU_SIMPLE || algo > MPGPU_WINOGRAD || param < 0)
+    return fail(h, MPGPU_ERR_DOMAIN, "unknown algorithm %d", algo);
+  if (C->rows != A->rows || C->cols != B->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "output shape mismatch");
+  if (A->prec != C->prec || B->prec != C->prec || A->nlimbs != C->nlimbs || B->nlimbs != C->nlimbs)
+    return fail(h, MPGPU_ERR_DOMAIN, "device GEMM requires one precision for A, B and C");
+  return MPGPU_OK;
+}
+
+// ---- host generators -----------------------------------------------------
+struct Prng64 {  // xorshift64* (matgen.hpp:13-42)
+  uint64_t s;
+  explicit Prng64(uint64_t seed) : s(seed ? seed : 0x9E3779B97F4A7C15ULL) {}
+  uint64_t next64() {
+    uint64_t x = s;
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    s = x;
+    return x * 2685821657736338717ULL;
+  }
+  uint64_t top53() { return next64() >> 11; }
+};
+
+// big integer (little-endian 32-bit words) helpers
+struct BitWriter {  // MSB-first bit stream into a big integer of `total` bits
+  std::vector<uint32_t> w;
+  int total, pos = 0;  // pos = bits written
+  explicit BitWriter(int bits) : w((bits + 31) / 32 + 1, 0), total(bits) {}
+  void put(uint64_t bits, int nb) {  // append nb (<= 53) bits, MSB first
+    for (int i = nb - 1; i >= 0;) {
+      // bit index from the LSB of the whole number
+      const int idx = total - 1 - pos;
+      const int word = idx >> 5, bit = idx & 31;
+      const int room = bit + 1;  // bits available in this word at and below `bit`
+      const int take = std::min(room, i + 1);
+      const uint32_t chunk = (uint32_t)((bits >> (i + 1 - take)) & ((1ull << take) - 1));
+      w[word] |= chunk << (bit + 1 - take);
+      pos += take;
+      i -= take;
+    }
+  }
+};
+
+// write a nonzero magnitude (big int, little-endian words, bit length b) as a
+// left-aligned L-limb mantissa; returns false if it would need rounding
+void put_mantissa(const std::vector<uint32_t>& v, int b, int Lh, int64_t N, int64_t e, uint32_t* limbs) {
+  // shift left so that bit (b-1) lands at bit (32*Lh - 1)
+  const int shift = 32 * Lh - b;  // may be negative only if b > 32*Lh (not for our inputs)
+  for (int k = 0; k < Lh; ++k) {
+    // output word k covers bits [32k, 32k+32) of (v << shift)
+    uint64_t acc = 0;
+    const int lo = 32 * k - shift;  // source bit index of output bit 32k
+    for (int t = 0; t < 32; ++t) {
+      const int sb = lo + t;
+      if (sb >= 0 && sb < (int)v.size() * 32) acc |= (uint64_t)((v[sb >> 5] >> (sb & 31)) & 1u) << t;
+    }
+    limbs[(int64_t)k * N + e] = (uint32_t)acc;
+  }
+}
+
+int bitlen(const std::vector<uint32_t>& v) {
+  for (int k = (int)v.size() - 1; k >= 0; --k)
+    if (v[k]) return 32 * k + 32 - __builtin_clz(v[k]);
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int mpgpu_init(int device, mpgpu_handle** out) {
+  if (!out) return MPGPU_ERR_DOMAIN;
+  *out = nullptr;
+  auto* h = new mpgpu_handle();
+  h->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_err, 4 * sizeof(uint32_t));  // [0] flags, [2:4) int64 zero pivot
+  if (e != cudaSuccess) {
+    delete h;
+    return MPGPU_ERR_CUDA;
+  }
+  h->stream = h->own_stream;
+  // keep freed pool memory cached: repeated calls reuse it without cudaMalloc
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = h;
+  return MPGPU_OK;
+}
+
+void mpgpu_destroy(mpgpu_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  if (h->d_err) cudaFree(h->d_err);
+  if (h->d_piv) cudaFree(h->d_piv);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+const char* mpgpu_last_error(const mpgpu_handle* h) { return h ? h->last_error.c_str() : "null handle"; }
+
+int mpgpu_set_stream(mpgpu_handle* h, void* s) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->stream = s ? static_cast<cudaStream_t>(s) : h->own_stream;
+  return MPGPU_OK;
+}
+
+void* mpgpu_get_stream(mpgpu_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int mpgpu_synchronize(mpgpu_handle* h) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return MPGPU_OK;
+}
+
+int mpgpu_nlimbs_for(int32_t prec) { return nlimbs_for(prec); }
+int mpgpu_record_words(int32_t nlimbs) { return rec_stride(nlimbs); }
+
+int mpgpu_alloc_matrix(mpgpu_handle* h, int64_t rows, int64_t cols, int32_t prec, mpgpu_mat* out) {
+  if (!h || !out) return MPGPU_ERR_DOMAIN;
+  if (rows < 1 || cols < 1) return fail(h, MPGPU_ERR_DIMENSION, "matrix dimensions must be at least 1x1");
+  const int L = nlimbs_for(prec);
+  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  void* p = nullptr;
+  const size_t bytes = sizeof(uint32_t) * (size_t)rec_stride(L) * (size_t)(rows * cols);
+  CUDA_TRY(h, cudaMalloc(&p, bytes));
+  // +0 everywhere (Matrix ctor, matrix.hpp:22-28: every element Scalar(ctx) = +0):
+  // all-zero words except the exponent word, set by the conversion kernel below.
+  CUDA_TRY(h, cudaMemsetAsync(p, 0, bytes, h->stream));
+  out->rows = rows;
+  out->cols = cols;
+  out->prec = prec;
+  out->nlimbs = L;
+  out->rec = static_cast<uint32_t*>(p);
+  out->ld = cols;
+  out->owned = 1;
+  // exponent words := EXP_ZERO
+  const int S = rec_stride(L);
+  CUDA_TRY(h, cudaMemset2DAsync(static_cast<uint32_t*>(p) + L, sizeof(uint32_t) * S, 0x00, 4, rows * cols,
+                                h->stream));
+  {
+    // write INT32_MIN (0x80000000): byte 3 of each exponent word = 0x80
+    CUDA_TRY(h, cudaMemset2DAsync(reinterpret_cast<uint8_t*>(static_cast<uint32_t*>(p) + L) + 3,
+                                  sizeof(uint32_t) * S, 0x80, 1, rows * cols, h->stream));
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return MPGPU_OK;
+}
+
+int mpgpu_free_matrix(mpgpu_handle* h, mpgpu_mat* m) {
+  if (!m) return MPGPU_OK;
+  if (m->owned && m->rec) {
+    if (h) cudaSetDevice(h->device);
+    cudaFree(m->rec);
+  }
+  m->rec = nullptr;
+  m->owned = 0;
+  return MPGPU_OK;
+}
+
+int mpgpu_upload(mpgpu_handle* h, mpgpu_mat* m, const uint32_t* limbs, const int32_t* exp, const uint8_t* sign,
+                 int32_t Lh) {
+  if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
+  if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "upload into a strided view");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  const int L = m->nlimbs;
+  const int64_t N = m->rows * m->cols;
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  DevBuf stage;
+  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
+  uint32_t* dl = stage.u32();
+  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
+  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
+  // most significant limbs aligned: host plane j <-> device plane j + (L - Lh)
+  if (Lh <= L) {
+    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
+                                cudaMemcpyHostToDevice, h->stream));
+  } else {
+    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, h->stream));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, h->stream));
+  dispatch_L(L, [&](auto Lc) {
+    mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, m->rec, h->stream);
+    return 0;
+  });
+  stage.release();
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int mpgpu_download(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                   int32_t Lh) {
+  if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
+  if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "download from a strided view");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  const int L = m->nlimbs;
+  const int64_t N = m->rows * m->cols;
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  DevBuf stage;
+  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
+  uint32_t* dl = stage.u32();
+  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
+  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
+  dispatch_L(L, [&](auto Lc) {
+    mpg::launch_rec2soa<decltype(Lc)::value>(m->rec, N, dl, de, ds, N, h->stream);
+    return 0;
+  });
+  if (Lh <= L) {
+    CUDA_TRY(h, cudaMemcpyAsync(limbs, dl + (size_t)(L - Lh) * N, sizeof(uint32_t) * (size_t)Lh * N,
+                                cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    std::memset(limbs, 0, sizeof(uint32_t) * (size_t)(Lh - L) * N);
+    CUDA_TRY(h, cudaMemcpyAsync(limbs + (size_t)(Lh - L) * N, dl, planes, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(exp, de, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(sign, ds, N, cudaMemcpyDeviceToHost, h->stream));
+  stage.release();
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int mpgpu_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C,
+               mpgpu_stats* stats) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  int rc = validate_gemm(h, algo, param, A, B, C);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  if (stats) {
+    std::memset(stats, 0, sizeof *stats);
+    uint64_t c[2];
+    count_fast_rec(algo, A->rows, A->cols, B->cols, param, c);
+    stats->mul = c[0];
+    stats->addsub = c[1];
+  }
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * C->nlimbs - C->prec;
+  rc = dispatch_L(C->nlimbs, [&](auto Lc) {
+    return run_gemm<decltype(Lc)::value>(h, algo, param, A->rec, A->ld, B->rec, B->ld, C->rec, C->ld, A->rows,
+                                         A->cols, B->cols, sh, stats, 0);
+  });
+  if (rc) return rc;
+  return check_err(h);
+}
+
+int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int64_t m, int64_t l, int64_t n,
+                    const uint32_t* al, const int32_t* ae, const uint8_t* as, const uint32_t* bl,
+                    const int32_t* be, const uint8_t* bs, uint32_t* cl, int32_t* ce, uint8_t* cs, int32_t Lh,
+                    mpgpu_stats* stats) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  mpgpu_mat A{}, B{}, C{};
+  int rc = mpgpu_alloc_matrix(h, m, l, prec, &A);
+  if (!rc) rc = mpgpu_alloc_matrix(h, l, n, prec, &B);
+  if (!rc) rc = mpgpu_alloc_matrix(h, m, n, prec, &C);
+  if (!rc) rc = mpgpu_upload(h, &A, al, ae, as, Lh);
+  if (!rc) rc = mpgpu_upload(h, &B, bl, be, bs, Lh);
+  if (!rc) rc = mpgpu_gemm(h, algo, param, &A, &B, &C, stats);
+  if (!rc) rc = mpgpu_download(h, &C, cl, ce, cs, Lh);
+  mpgpu_free_matrix(h, &A);
+  mpgpu_free_matrix(h, &B);
+  mpgpu_free_matrix(h, &C);
+  return rc;
+}
+
+int mpgpu_addsub(mpgpu_handle* h, int is_sub, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C) {
+  if (!h || !A || !B || !C) return MPGPU_ERR_DOMAIN;
+  if (A->prec != B->prec) return fail(h, MPGPU_ERR_DOMAIN, is_sub ? "mat sub: mixed precisions" : "mat add: mixed precisions");
+  if (A->rows != B->rows || A->cols != B->cols || C->rows != A->rows || C->cols != A->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "shape mismatch: %lldx%lld vs %lldx%lld", (long long)A->rows,
+                (long long)A->cols, (long long)B->rows, (long long)B->cols);
+  if (C->prec != A->prec || A->ld != A->cols || B->ld != B->cols || C->ld != C->cols)
+    return fail(h, MPGPU_ERR_DOMAIN, "addsub requires dense matrices of one precision");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * C->nlimbs - C->prec;
+  dispatch_L(C->nlimbs, [&](auto Lc) {
+    mpg::launch_addsub<decltype(Lc)::value>(A->rec, B->rec, C->rec, A->rows * A->cols, is_sub, sh, h->d_err,
+                                            h->stream);
+    return 0;
+  });
+  return check_err(h);
+}
+
+int mpgpu_vec_op(mpgpu_handle* h, int op, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C) {
+  if (!h || !A || !B || !C) return MPGPU_ERR_DOMAIN;
+  if (A->rows * A->cols != B->rows * B->cols || C->rows * C->cols != A->rows * A->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "vec_op: size mismatch");
+  if (A->prec != C->prec || B->prec != C->prec) return fail(h, MPGPU_ERR_DOMAIN, "vec_op: mixed precisions");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * C->nlimbs - C->prec;
+  dispatch_L(C->nlimbs, [&](auto Lc) {
+    mpg::launch_vec_op<decltype(Lc)::value>(op, A->rec, B->rec, C->rec, A->rows * A->cols, sh, h->d_err,
+                                            h->stream);
+    return 0;
+  });
+  return check_err(h);
+}
+
+int mpgpu_fast_mul_trace(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                         mpgpu_mat* C, uint32_t* trace_rec, int* counts) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  int rc = validate_gemm(h, algo, n_min, A, B, C);
+  if (rc) return rc;
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
+    return fail(h, MPGPU_ERR_DOMAIN, "fast_mul: algorithm must be strassen or winograd");
+  if (A->ld != A->cols || B->ld != B->cols || C->ld != C->cols)
+    return fail(h, MPGPU_ERR_DOMAIN, "trace requires dense matrices");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int64_t m = A->rows, l = A->cols, n = B->cols;
+  counts[0] = counts[1] = counts[2] = 0;
+  const int sh = 32 * C->nlimbs - C->prec;
+  if (std::min({m, l, n}) <= n_min) {  // base case: no trace (fastmm.hpp:102)
+    rc = dispatch_L(C->nlimbs, [&](auto Lc) {
+      return run_gemm<decltype(Lc)::value>(h, MPGPU_SIMPLE, 0, A->rec, m, B->rec, n, C->rec, n, m, l, n, sh,
+                                           nullptr, 0);
+    });
+    return rc ? rc : check_err(h);
+  }
+  const int64_t hm = (m + m % 2) / 2, hl = (l + l % 2) / 2, hn = (n + n % 2) / 2;
+  rc = dispatch_L(C->nlimbs, [&](auto Lc) -> int {
+    constexpr int L = decltype(Lc)::value;
+    constexpr int S = rec_stride(L);
+    cudaStream_t st = h->stream;
+    DevBuf ca, cb, prods;
+    CUDA_TRY(h, ca.alloc(h, sizeof(uint32_t) * S * 7 * hm * hl));
+    CUDA_TRY(h, cb.alloc(h, sizeof(uint32_t) * S * 7 * hl * hn));
+    CUDA_TRY(h, prods.alloc(h, sizeof(uint32_t) * S * 7 * hm * hn));
+    mpg::launch_preadd<L>(algo, 0, A->rec, 1, (int)m, (int)l, ca.u32(), sh, h->d_err, st);
+    mpg::launch_preadd<L>(algo, 1, B->rec, 1, (int)l, (int)n, cb.u32(), sh, h->d_err, st);
+    // the 7 children via the full driver (each is a fast_mul_rec call)
+    for (int q = 0; q < 7; ++q) {
+      int r = run_gemm<L>(h, algo, n_min, ca.u32() + (size_t)q * S * hm * hl, hl, cb.u32() + (size_t)q * S * hl * hn,
+                          hn, prods.u32() + (size_t)q * S * hm * hn, hn, hm, hl, hn, sh, nullptr, 0);
+      if (r) return r;
+    }
+    uint32_t* tout = trace_rec;
+    int64_t off = 0;
+    const size_t ha = (size_t)hm * hl, hb = (size_t)hl * hn, hp = (size_t)hm * hn;
+    auto cpy = [&](const uint32_t* src, size_t elems) {
+      cudaMemcpyAsync(tout + off * S, src, sizeof(uint32_t) * S * elems, cudaMemcpyDeviceToDevice, st);
+      off += (int64_t)elems;
+    };
+    uint32_t* t_out = nullptr;
+    if (algo == MPGPU_WINOGRAD) {
+      // S1..S4 are children A operands 4,0,3,5; S5..S8 children B operands 4,0,3,6
+      const int sa[4] = {4, 0, 3, 5}, sb[4] = {4, 0, 3, 6};
+      for (int q : sa) cpy(ca.u32() + q * S * ha, ha);
+      for (int q : sb) cpy(cb.u32() + q * S * hb, hb);
+      counts[0] = 8;
+    }
+    for (int q = 0; q < 7; ++q) cpy(prods.u32() + q * S * hp, hp);
+    counts[1] = 7;
+    if (algo == MPGPU_WINOGRAD) {
+      t_out = tout + off * S;
+      counts[2] = 2;
+    }
+    mpg::launch_postadd<L>(algo, prods.u32(), 1, (int)m, (int)n, C->rec, t_out, sh, h->d_err, st);
+    return 0;
+  });
+  if (rc) return rc;
+  return check_err(h);
+}
+
+int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min, int pivoting,
+                     int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats) {
+  if (!h || !A) return MPGPU_ERR_DOMAIN;
+  if (zero_pivot) *zero_pivot = 0;
+  if (A->rows != A->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: matrix must be square");
+  if (K == 0) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: block size must be at least 1");
+  if (A->ld != A->cols) return fail(h, MPGPU_ERR_DOMAIN, "lu_blocked: dense matrix required");
+  const int64_t n = A->rows;
+  if (n > K && kernel != MPGPU_SIMPLE && n_min == 0)
+    return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
+  if (kernel < MPGPU_SIMPLE || kernel > MPGPU_WINOGRAD) return fail(h, MPGPU_ERR_DOMAIN, "unknown kernel");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  if (stats) std::memset(stats, 0, sizeof *stats);
+  if (pivoting && h->d_piv_cap < n) {
+    if (h->d_piv) cudaFree(h->d_piv);
+    h->d_piv = nullptr;
+    CUDA_TRY(h, cudaMalloc(&h->d_piv, sizeof(int64_t) * n));
+    h->d_piv_cap = n;
+  }
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * A->nlimbs - A->prec;
+  int64_t* zp = reinterpret_cast<int64_t*>(h->d_err + 2);
+  Timer total(stats != nullptr, h->stream);
+  int rc = dispatch_L(A->nlimbs, [&](auto Lc) -> int {
+    constexpr int L = decltype(Lc)::value;
+    constexpr int S = rec_stride(L);
+    cudaStream_t st = h->stream;
+    uint32_t* a = A->rec;
+    int64_t off = 0;
+    auto panel = [&](int64_t p, int64_t k) {
+      for (int64_t d = p; d < p + k; ++d) {
+        if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, st);
+        mpg::launch_lu_step<L>(a, n, d, n, p + k, sh, h->d_err, st);
+      }
+    };
+    while (n - off > K) {
+      const int64_t rest = n - off - K;
+      panel(off, K);
+      for (int64_t s = off; s + 1 < off + K; ++s)
+        mpg::launch_trsm_l_step<L>(a, n, s, off + K, off + K, rest, sh, h->d_err, st);
+      const uint32_t* l21 = a + ((off + K) * n + off) * S;
+      const uint32_t* u12 = a + (off * n + off + K) * S;
+      uint32_t* a22 = a + ((off + K) * n + off + K) * S;
+      mpgpu_stats ss{};
+      if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) {
+        int r = run_gemm<L>(h, kernel, n_min, l21, n, u12, n, a22, n, rest, K, rest, sh, stats ? &ss : nullptr, 1);
+        if (r) return r;
+      } else {
+        DevBuf prod;
+        CUDA_TRY(h, prod.alloc(h, sizeof(uint32_t) * S * rest * rest));
+        int r = run_gemm<L>(h, kernel, n_min, l21, n, u12, n, prod.u32(), rest, rest, K, rest, sh,
+                            stats ? &ss : nullptr, 0);
+        if (r) return r;
+        mpg::launch_sub2d<L>(a22, n, prod.u32(), (int)rest, (int)rest, sh, h->d_err, st);
+      }
+      if (stats) {
+        uint64_t c[2];
+        count_fast_rec(kernel, rest, K, rest, n_min, c);
+        stats->mul += c[0];
+        stats->addsub += c[1];
+        stats->leaf_ms += ss.leaf_ms;
+        stats->leaf_madds += ss.leaf_madds;
+        stats->launches += ss.launches;
+      }
+      off += K;
+    }
+    panel(off, n - off);
+    return 0;
+  });
+  if (stats) stats->device_ms = total.stop();
+  if (rc) return rc;
+  int64_t zpv = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&zpv, zp, sizeof zpv, cudaMemcpyDeviceToHost, h->stream));
+  if (pivoting && piv_out)
+    CUDA_TRY(h, cudaMemcpyAsync(piv_out, h->d_piv, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, h->stream));
+  rc = check_err(h);
+  if (zpv) {
+    if (zero_pivot) *zero_pivot = zpv;
+    return fail(h, MPGPU_ERR_SINGULAR, "zero pivot at index %lld", (long long)zpv);
+  }
+  return rc;
+}
+
+int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
+                   int64_t* zero_pivot) {
+  if (!h || !F || !b || !x) return MPGPU_ERR_DOMAIN;
+  if (zero_pivot) *zero_pivot = 0;
+  const int64_t n = F->rows;
+  if (F->rows != F->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: factors must be square");
+  if (b->rows * b->cols != n || x->rows * x->cols != n) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: length mismatch");
+  if (b->prec != F->prec || x->prec != F->prec) return fail(h, MPGPU_ERR_DOMAIN, "lu_solve: mixed precisions");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  int64_t* zp = reinterpret_cast<int64_t*>(h->d_err + 2);
+  DevBuf dpiv, scratch;
+  if (piv) {
+    CUDA_TRY(h, dpiv.alloc(h, sizeof(int64_t) * n));
+    CUDA_TRY(h, cudaMemcpyAsync(dpiv.p, piv, sizeof(int64_t) * n, cudaMemcpyHostToDevice, h->stream));
+  }
+  const int sh = 32 * F->nlimbs - F->prec;
+  int rc = dispatch_L(F->nlimbs, [&](auto Lc) -> int {
+    constexpr int L = decltype(Lc)::value;
+    CUDA_TRY(h, scratch.alloc(h, sizeof(uint32_t) * rec_stride(L) * 2 * n));
+    mpg::launch_lu_solve<L>(F->rec, n, piv ? static_cast<const int64_t*>(dpiv.p) : nullptr, b->rec, x->rec,
+                            scratch.u32(), sh, h->d_err, zp, h->stream);
+    return 0;
+  });
+  if (rc) return rc;
+  int64_t zpv = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&zpv, zp, sizeof zpv, cudaMemcpyDeviceToHost, h->stream));
+  rc = check_err(h);
+  if (zpv) {
+    if (zero_pivot) *zero_pivot = zpv;
+    return fail(h, MPGPU_ERR_SINGULAR, "zero pivot at index %lld", (long long)zpv);
+  }
+  return rc;
+}
+
+int mpgpu_count_fast(int algo, int64_t m, int64_t l, int64_t n, int64_t n_min, uint64_t* out2) {
+  if (m < 1 || l < 1 || n < 1) return MPGPU_ERR_DIMENSION;
+  if (n_min == 0 && algo >= MPGPU_STRASSEN) return MPGPU_ERR_DIMENSION;
+  count_fast_rec(algo, m, l, n, n_min, out2);
+  return MPGPU_OK;
+}
+
+int mpgpu_recursion_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out, int max_levels, int* count) {
+  if (n_min == 0) return MPGPU_ERR_DIMENSION;
+  int lev = 0;
+  for (;;) {
+    const bool base = std::min({m, l, n}) <= n_min;
+    const int64_t pm = base ? m : m + m % 2, pl = base ? l : l + l % 2, pn = base ? n : n + n % 2;
+    if (lev < max_levels) {
+      int64_t* r = out + 8 * lev;
+      r[0] = lev;
+      r[1] = m;
+      r[2] = l;
+      r[3] = n;
+      r[4] = pm;
+      r[5] = pl;
+      r[6] = pn;
+      r[7] = base;
+    }
+    ++lev;
+    if (base) break;
+    m = pm / 2;
+    l = pl / 2;
+    n = pn / 2;
+  }
+  *count = lev;
+  return MPGPU_OK;
+}
+
+int mpgpu_gen(int kind, int64_t N, uint64_t seed, int32_t prec, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+              int32_t Lh) {
+  if (prec < 2 || Lh < (prec + 31) / 32) return MPGPU_ERR_DOMAIN;
+  Prng64 rng(seed);
+  for (int64_t e = 0; e < N; ++e) {
+    if (kind == 0) {
+      // num = 2 k - 2^53 (|num| <= 2^53), value = RN_p(num) * 2^-53
+      const int64_t num = (int64_t)(2 * rng.top53()) - ((int64_t)1 << 53);
+      sign[e] = num < 0;
+      uint64_t u = num < 0 ? (uint64_t)(-num) : (uint64_t)num;
+      if (u == 0) {
+        for (int k = 0; k < Lh; ++k) limbs[(int64_t)k * N + e] = 0;
+        exp[e] = MPGPU_EXP_ZERO;
+        sign[e] = 0;
+        continue;
+      }
+      const int b = 64 - __builtin_clzll(u);
+      int32_t ex = b - 53;
+      uint64_t M = u << (64 - b);  // left aligned
+      if (prec < 64) {
+        const int drop = 64 - prec;
+        const uint64_t low = M & ((1ull << drop) - 1);
+        const uint64_t half = 1ull << (drop - 1);
+        M -= low;
+        const bool up = low > half || (low == half && ((M >> drop) & 1));
+        if (up) {
+          M += 1ull << drop;
+          if (M == 0) {  // carried out
+            M = 1ull << 63;
+            ex += 1;
+          }
+        }
+      }
+      for (int k = 0; k < Lh; ++k) limbs[(int64_t)k * N + e] = 0;
+      limbs[(int64_t)(Lh - 1) * N + e] = (uint32_t)(M >> 32);
+      if (Lh >= 2) limbs[(int64_t)(Lh - 2) * N + e] = (uint32_t)M;
+      exp[e] = ex;
+    } else if (kind == 1) {
+      const int need = prec + 1;
+      BitWriter bw(need);
+      for (int have = 0; have < need;) {
+        const uint64_t d = rng.top53();
+        const int take = std::min(53, need - have);
+        bw.put(d >> (53 - take), take);
+        have += take;
+      }
+      std::vector<uint32_t>& K = bw.w;
+      const bool ge = (K[prec >> 5] >> (prec & 31)) & 1u;  // bit p: k >= 2^p
+      std::vector<uint32_t> v(K.size(), 0);
+      if (ge) {
+        v = K;
+        v[prec >> 5] &= ~(1u << (prec & 31));
+      } else {  // v = 2^p - k
+        std::vector<uint32_t> two(K.size(), 0);
+        two[prec >> 5] = 1u << (prec & 31);
+        uint64_t borrow = 0;
+        for (size_t k = 0; k < K.size(); ++k) {
+          const uint64_t t = (uint64_t)two[k] - K[k] - borrow;
+          v[k] = (uint32_t)t;
+          borrow = (t >> 63) & 1;
+        }
+      }
+      const int b = bitlen(v);
+      if (b == 0) {
+        for (int k = 0; k < Lh; ++k) limbs[(int64_t)k * N + e] = 0;
+        exp[e] = MPGPU_EXP_ZERO;
+        sign[e] = 0;
+        continue;
+      }
+      put_mantissa(v, b, Lh, N, e, limbs);
+      exp[e] = b - prec;
+      sign[e] = ge ? 0 : 1;
+    } else {
+      const uint32_t sg = (uint32_t)(rng.next64() >> 63);
+      const int32_t ex = (int32_t)(rng.next64() % 41) - 20;
+      const int need = prec - 1;
+      BitWriter bw(prec);
+      bw.put(1, 1);  // leading one
+      for (int have = 0; have < need;) {
+        const uint64_t d = rng.top53();
+        const int take = std::min(53, need - have);
+        bw.put(d >> (53 - take), take);
+        have += take;
+      }
+      put_mantissa(bw.w, prec, Lh, N, e, limbs);
+      exp[e] = ex;
+      sign[e] = (uint8_t)sg;
+    }
+  }
+  return MPGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,392 @@
+// elementwise.cu -- HBM-bound MP kernels: layout conversion, add/sub, and the
+// fused Strassen / Winograd level transforms (K2 mp_preadd, K3 mp_postadd).
+//
+// Pre-add (fastmm.hpp:104-115 pad + quadrants, :134-150 Strassen sums,
+// :173-180 Winograd S1..S8): one thread per (parent node, quadrant element),
+// reads the four quadrant records (virtual zero padding for odd dimensions --
+// pad_operand, fastmm.hpp:91-97, fills +0), forms the sums with the reference's
+// operand order and writes the seven child operands.  Post-add (fastmm.hpp:152-161
+// Strassen, :190-198 Winograd, :221-227 strip): one thread per (parent, element)
+// reads the seven child products and writes the four C quadrants, dropping padded
+// rows/columns.  Every sum is the same correctly rounded MP add as the reference's
+// addsub (matrix.hpp:121-134), so fusing them is bit-exact.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "mp_arith.cuh"
+
+namespace mpg {
+
+namespace {
+constexpr int NT = 256;
+inline int grid_for(int64_t n) {
+  int64_t b = (n + NT - 1) / NT;
+  return (int)(b < 148 * 64 ? (b < 1 ? 1 : b) : 148 * 64);
+}
+}  // namespace
+
+template <int L>
+__global__ void soa2rec_kernel(const uint32_t* __restrict__ limbs, const int32_t* __restrict__ exp,
+                               const uint8_t* __restrict__ sign, int64_t N, int64_t ps,
+                               uint32_t* __restrict__ rec) {
+  constexpr int S = rec_stride(L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    MP<L> x;
+#pragma unroll
+    for (int k = 0; k < L; ++k) x.m[k] = limbs[k * ps + e];
+    x.e = exp[e];
+    x.s = sign[e];
+    store_rec<L>(rec + e * S, x);
+  }
+}
+
+template <int L>
+__global__ void rec2soa_kernel(const uint32_t* __restrict__ rec, int64_t N, uint32_t* __restrict__ limbs,
+                               int32_t* __restrict__ exp, uint8_t* __restrict__ sign, int64_t ps) {
+  constexpr int S = rec_stride(L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    MP<L> x;
+    load_rec<L>(rec + e * S, x);
+#pragma unroll
+    for (int k = 0; k < L; ++k) limbs[k * ps + e] = x.m[k];
+    exp[e] = x.e;
+    sign[e] = (uint8_t)x.s;
+  }
+}
+
+template <int L>
+__global__ void addsub_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                              uint32_t* __restrict__ C, int64_t N, uint32_t neg, int sh,
+                              uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    MP<L> a, b, c;
+    load_rec<L>(A + e * S, a);
+    load_rec<L>(B + e * S, b);
+    mp_add<L>(a, b, neg, sh, c);
+    if (exp_out_of_range(c.e)) atomicOr(err, ERR_EXP_RANGE);
+    store_rec<L>(C + e * S, c);
+  }
+}
+
+template <int L>
+__global__ void vec_op_kernel(int op, const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                              uint32_t* __restrict__ C, int64_t N, int sh, uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    MP<L> a, b, c;
+    load_rec<L>(A + e * S, a);
+    load_rec<L>(B + e * S, b);
+    if (op == 0)
+      mp_add<L>(a, b, 0u, sh, c);
+    else if (op == 1)
+      mp_add<L>(a, b, 1u, sh, c);
+    else if (op == 2)
+      mp_mul<L>(a, b, sh, c);
+    else {
+      if (b.e == EXP_ZERO) {
+        atomicOr(err, ERR_DIV_ZERO);
+        mp_zero(c);
+      } else {
+        mp_div<L>(a, b, sh, c);
+      }
+    }
+    if (exp_out_of_range(c.e)) atomicOr(err, ERR_EXP_RANGE);
+    store_rec<L>(C + e * S, c);
+  }
+}
+
+// read parent element (r, c) of a rows x cols dense record matrix, +0 outside
+template <int L>
+__device__ __forceinline__ void load_padded(const uint32_t* P, int rows, int cols, int r, int c, MP<L>& x) {
+  if (r < rows && c < cols)
+    load_rec<L>(P + ((int64_t)r * cols + c) * rec_stride(L), x);
+  else
+    mp_zero(x, 0);
+}
+
+template <int L>
+__global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
+                              int rows, int cols, uint32_t* __restrict__ children, int sh) {
+  constexpr int S = rec_stride(L);
+  const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
+  const int64_t per = (int64_t)hr * hc;
+  const int64_t total = per * nodes;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = t / per;
+    const int64_t e = t - node * per;
+    const int r = (int)(e / hc), c = (int)(e - (int64_t)r * hc);
+    const uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    MP<L> x11, x12, x21, x22;
+    load_padded<L>(P, rows, cols, r, c, x11);
+    load_padded<L>(P, rows, cols, r, c + hc, x12);
+    load_padded<L>(P, rows, cols, r + hr, c, x21);
+    load_padded<L>(P, rows, cols, r + hr, c + hc, x22);
+    uint32_t* out = children + (node * 7 * per + e) * S;
+    const int64_t cs = per * S;  // stride between sibling children
+    if (algo == 3) {
+      if (side == 0) {  // S1 = a21+a22, S2 = S1-a11, S3 = a11-a21, S4 = a12-S2
+        MP<L> s1, s2, s3, s4;
+        mp_add<L>(x21, x22, 0u, sh, s1);
+        mp_add<L>(s1, x11, 1u, sh, s2);
+        mp_add<L>(x11, x21, 1u, sh, s3);
+        mp_add<L>(x12, s2, 1u, sh, s4);
+        store_rec<L>(out + 0 * cs, s2);   // M1 = S2*S6
+        store_rec<L>(out + 1 * cs, x11);  // M2 = a11*b11
+        store_rec<L>(out + 2 * cs, x12);  // M3 = a12*b21
+        store_rec<L>(out + 3 * cs, s3);   // M4 = S3*S7
+        store_rec<L>(out + 4 * cs, s1);   // M5 = S1*S5
+        store_rec<L>(out + 5 * cs, s4);   // M6 = S4*b22
+        store_rec<L>(out + 6 * cs, x22);  // M7 = a22*S8
+      } else {  // S5 = b12-b11, S6 = b22-S5, S7 = b22-b12, S8 = S6-b21
+        MP<L> s5, s6, s7, s8;
+        mp_add<L>(x12, x11, 1u, sh, s5);
+        mp_add<L>(x22, s5, 1u, sh, s6);
+        mp_add<L>(x22, x12, 1u, sh, s7);
+        mp_add<L>(s6, x21, 1u, sh, s8);
+        store_rec<L>(out + 0 * cs, s6);
+        store_rec<L>(out + 1 * cs, x11);
+        store_rec<L>(out + 2 * cs, x21);
+        store_rec<L>(out + 3 * cs, s7);
+        store_rec<L>(out + 4 * cs, s5);
+        store_rec<L>(out + 5 * cs, x22);
+        store_rec<L>(out + 6 * cs, s8);
+      }
+    } else {
+      MP<L> u;
+      if (side == 0) {  // a11+a22, a21+a22, a11, a22, a11+a12, a21-a11, a12-a22
+        mp_add<L>(x11, x22, 0u, sh, u);
+        store_rec<L>(out + 0 * cs, u);
+        mp_add<L>(x21, x22, 0u, sh, u);
+        store_rec<L>(out + 1 * cs, u);
+        store_rec<L>(out + 2 * cs, x11);
+        store_rec<L>(out + 3 * cs, x22);
+        mp_add<L>(x11, x12, 0u, sh, u);
+        store_rec<L>(out + 4 * cs, u);
+        mp_add<L>(x21, x11, 1u, sh, u);
+        store_rec<L>(out + 5 * cs, u);
+        mp_add<L>(x12, x22, 1u, sh, u);
+        store_rec<L>(out + 6 * cs, u);
+      } else {  // b11+b22, b11, b12-b22, b21-b11, b22, b11+b12, b21+b22
+        mp_add<L>(x11, x22, 0u, sh, u);
+        store_rec<L>(out + 0 * cs, u);
+        store_rec<L>(out + 1 * cs, x11);
+        mp_add<L>(x12, x22, 1u, sh, u);
+        store_rec<L>(out + 2 * cs, u);
+        mp_add<L>(x21, x11, 1u, sh, u);
+        store_rec<L>(out + 3 * cs, u);
+        store_rec<L>(out + 4 * cs, x22);
+        mp_add<L>(x11, x12, 0u, sh, u);
+        store_rec<L>(out + 5 * cs, u);
+        mp_add<L>(x21, x22, 0u, sh, u);
+        store_rec<L>(out + 6 * cs, u);
+      }
+    }
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r, int c, const MP<L>& x,
+                                         uint32_t* err) {
+  if (r < rows && c < cols) {
+    if (exp_out_of_range(x.e)) atomicOr(err, ERR_EXP_RANGE);
+    store_rec<L>(P + ((int64_t)r * cols + c) * rec_stride(L), x);
+  }
+}
+
+template <int L>
+__global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
+                               int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
+                               int sh, uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
+  const int64_t per = (int64_t)hr * hc;
+  const int64_t total = per * nodes;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = t / per;
+    const int64_t e = t - node * per;
+    const int r = (int)(e / hc), c = (int)(e - (int64_t)r * hc);
+    const uint32_t* M = children + (node * 7 * per + e) * S;
+    const int64_t cs = per * S;
+    uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    if (algo == 3) {
+      // T1 = M1+M2, T2 = T1+M4; C11 = M2+M3, C12 = (T1+M5)+M6, C21 = T2-M7, C22 = T2+M5
+      MP<L> m1, m2, t1, t2, u, v;
+      load_rec<L>(M + 0 * cs, m1);
+      load_rec<L>(M + 1 * cs, m2);
+      mp_add<L>(m1, m2, 0u, sh, t1);
+      {
+        MP<L> m4;
+        load_rec<L>(M + 3 * cs, m4);
+        mp_add<L>(t1, m4, 0u, sh, t2);
+      }
+      if (t_out) {
+        store_rec<L>(t_out + (node * 2 * per + e) * S, t1);
+        store_rec<L>(t_out + (node * 2 * per + per + e) * S, t2);
+      }
+      {
+        MP<L> m3;
+        load_rec<L>(M + 2 * cs, m3);
+        mp_add<L>(m2, m3, 0u, sh, u);
+        store_if<L>(P, rows, cols, r, c, u, err);
+      }
+      MP<L> m5;
+      load_rec<L>(M + 4 * cs, m5);
+      {
+        MP<L> m6;
+        load_rec<L>(M + 5 * cs, m6);
+        mp_add<L>(t1, m5, 0u, sh, u);
+        mp_add<L>(u, m6, 0u, sh, v);
+        store_if<L>(P, rows, cols, r, c + hc, v, err);
+      }
+      {
+        MP<L> m7;
+        load_rec<L>(M + 6 * cs, m7);
+        mp_add<L>(t2, m7, 1u, sh, u);
+        store_if<L>(P, rows, cols, r + hr, c, u, err);
+      }
+      mp_add<L>(t2, m5, 0u, sh, u);
+      store_if<L>(P, rows, cols, r + hr, c + hc, u, err);
+    } else {
+      // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
+      MP<L> p1, p4, p5, u, v;
+      load_rec<L>(M + 0 * cs, p1);
+      load_rec<L>(M + 3 * cs, p4);
+      load_rec<L>(M + 4 * cs, p5);
+      mp_add<L>(p1, p4, 0u, sh, u);
+      mp_add<L>(u, p5, 1u, sh, v);
+      {
+        MP<L> p7;
+        load_rec<L>(M + 6 * cs, p7);
+        mp_add<L>(v, p7, 0u, sh, u);
+        store_if<L>(P, rows, cols, r, c, u, err);
+      }
+      MP<L> p3;
+      load_rec<L>(M + 2 * cs, p3);
+      mp_add<L>(p3, p5, 0u, sh, u);
+      store_if<L>(P, rows, cols, r, c + hc, u, err);
+      MP<L> p2;
+      load_rec<L>(M + 1 * cs, p2);
+      mp_add<L>(p2, p4, 0u, sh, u);
+      store_if<L>(P, rows, cols, r + hr, c, u, err);
+      mp_add<L>(p1, p3, 0u, sh, u);
+      mp_add<L>(u, p2, 1u, sh, v);
+      {
+        MP<L> p6;
+        load_rec<L>(M + 5 * cs, p6);
+        mp_add<L>(v, p6, 0u, sh, u);
+        store_if<L>(P, rows, cols, r + hr, c + hc, u, err);
+      }
+    }
+  }
+}
+
+template <int L>
+__global__ void copy2d_kernel(const uint32_t* __restrict__ src, int64_t lds, uint32_t* __restrict__ dst,
+                              int64_t ldd, int rows, int cols) {
+  constexpr int S = rec_stride(L);
+  constexpr int CH = S / 4;
+  const int64_t total = (int64_t)rows * cols * CH;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / CH;
+    const int w = (int)(t - e * CH);
+    const int r = (int)(e / cols), c = (int)(e - (int64_t)r * cols);
+    *reinterpret_cast<uint4*>(dst + (r * ldd + c) * S + 4 * w) =
+        *reinterpret_cast<const uint4*>(src + (r * lds + c) * S + 4 * w);
+  }
+}
+
+template <int L>
+__global__ void sub2d_kernel(uint32_t* __restrict__ C, int64_t ldc, const uint32_t* __restrict__ T, int rows,
+                             int cols, int sh, uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / cols, c = t - r * cols;
+    MP<L> x, y, z;
+    load_rec<L>(C + (r * ldc + c) * S, x);
+    load_rec<L>(T + t * S, y);
+    mp_add<L>(x, y, 1u, sh, z);
+    if (exp_out_of_range(z.e)) atomicOr(err, ERR_EXP_RANGE);
+    store_rec<L>(C + (r * ldc + c) * S, z);
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int L>
+void launch_sub2d(uint32_t* C, int64_t ldc, const uint32_t* T, int rows, int cols, int sh, uint32_t* err,
+                  cudaStream_t st) {
+  sub2d_kernel<L><<<grid_for((int64_t)rows * cols), NT, 0, st>>>(C, ldc, T, rows, cols, sh, err);
+}
+template <int L>
+void launch_soa2rec(const uint32_t* limbs, const int32_t* exp, const uint8_t* sign, int64_t N,
+                    int64_t ps, uint32_t* rec, cudaStream_t st) {
+  soa2rec_kernel<L><<<grid_for(N), NT, 0, st>>>(limbs, exp, sign, N, ps, rec);
+}
+template <int L>
+void launch_rec2soa(const uint32_t* rec, int64_t N, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                    int64_t ps, cudaStream_t st) {
+  rec2soa_kernel<L><<<grid_for(N), NT, 0, st>>>(rec, N, limbs, exp, sign, ps);
+}
+template <int L>
+void launch_addsub(const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int is_sub, int sh,
+                   uint32_t* err, cudaStream_t st) {
+  addsub_kernel<L><<<grid_for(N), NT, 0, st>>>(A, B, C, N, is_sub ? 1u : 0u, sh, err);
+}
+template <int L>
+void launch_vec_op(int op, const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int sh,
+                   uint32_t* err, cudaStream_t st) {
+  vec_op_kernel<L><<<grid_for(N), NT, 0, st>>>(op, A, B, C, N, sh, err);
+}
+template <int L>
+void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
+                   uint32_t* children, int sh, uint32_t* err, cudaStream_t st) {
+  (void)err;
+  const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh);
+}
+template <int L>
+void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
+                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st) {
+  const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,
+                                                     err);
+}
+template <int L>
+void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
+                   cudaStream_t st) {
+  const int64_t total = (int64_t)rows * cols * (rec_stride(L) / 4);
+  copy2d_kernel<L><<<grid_for(total), NT, 0, st>>>(src, lds, dst, ldd, rows, cols);
+}
+
+#define MPG_INST(L)                                                                                     \
+  template void launch_soa2rec<L>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t,   \
+                                  uint32_t*, cudaStream_t);                                             \
+  template void launch_rec2soa<L>(const uint32_t*, int64_t, uint32_t*, int32_t*, uint8_t*, int64_t,    \
+                                  cudaStream_t);                                                        \
+  template void launch_addsub<L>(const uint32_t*, const uint32_t*, uint32_t*, int64_t, int, int,        \
+                                 uint32_t*, cudaStream_t);                                              \
+  template void launch_vec_op<L>(int, const uint32_t*, const uint32_t*, uint32_t*, int64_t, int,        \
+                                 uint32_t*, cudaStream_t);                                              \
+  template void launch_preadd<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int,          \
+                                 uint32_t*, cudaStream_t);                                              \
+  template void launch_postadd<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, uint32_t*, int,   \
+                                  uint32_t*, cudaStream_t);                                             \
+  template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
+  template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);
+MPG_INST(1)
+MPG_INST(2)
+MPG_INST(4)
+MPG_INST(8)
+MPG_INST(16)
+MPG_INST(32)
+
+}  // namespace mpg

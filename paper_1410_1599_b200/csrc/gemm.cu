@@ -1,0 +1,197 @@
+// gemm.cu -- K1 mp_gemm_leaf: batched MP GEMM leaf kernel for sm_100a.
+//
+// Replaces the reference's hot loop detail::mul_views (matrix.hpp:147-155) and the
+// Block tile loop block_mul_impl (matrix.hpp:196-216):
+//   c_ij = RN(..RN(RN(a_i0 b_0j) + RN(a_i1 b_1j))..)   left to right in k
+// and, with a k-tile kb < l, a fresh accumulator per k-tile followed by
+// C = RN(C + P).  One thread owns one output element: the k order inside an
+// element is sequential (no split-K -- reassociation would change the rounding),
+// parallelism comes from outputs and from the batch of leaves (grid.z).
+//
+// Operands are AoS records (rec_stride(L) words: limbs, exp, sign, pad) staged
+// through shared memory with cp.async (16-byte, zero-fill outside the matrix) in a
+// two-stage pipeline.  A warp covers 2 rows x 16 columns of C: the a-record of
+// each k is a broadcast LDS.128, the 16 b-records are consecutive records whose
+// stride/4 is odd, so the LDS.128 quarter-warps are bank-conflict free.
+// Limb products are IMAD / IMAD.HI on the FMA pipe (mp_arith.cuh).
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "mp_arith.cuh"
+
+namespace mpg {
+
+__device__ __forceinline__ void cp_async16(uint32_t* sdst, const uint32_t* gsrc, int src_bytes) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gsrc),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int L>
+struct GemmCfg;
+template <>
+struct GemmCfg<1> {
+  static constexpr int TM = 16, TN = 16, TK = 16;
+};
+template <>
+struct GemmCfg<2> {
+  static constexpr int TM = 16, TN = 16, TK = 16;
+};
+template <>
+struct GemmCfg<4> {
+  static constexpr int TM = 16, TN = 16, TK = 16;
+};
+template <>
+struct GemmCfg<8> {
+  static constexpr int TM = 16, TN = 16, TK = 16;
+};
+template <>
+struct GemmCfg<16> {
+  static constexpr int TM = 8, TN = 16, TK = 8;
+};
+template <>
+struct GemmCfg<32> {
+  static constexpr int TM = 8, TN = 16, TK = 4;
+};
+
+template <int L, int TM, int TN, int TK>
+__global__ void __launch_bounds__(TM* TN) gemm_leaf_kernel(const GemmArgs g) {
+  constexpr int S = rec_stride(L);
+  constexpr int NT = TM * TN;
+  constexpr int A_WORDS = TM * TK * S, B_WORDS = TK * TN * S;
+  constexpr bool A_STREAM = (L >= 16);  // large L: a-limbs read from smem inside the product
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* sA = smem;
+  uint32_t* sB = smem + 2 * A_WORDS;
+
+  const int tid = threadIdx.x, tx = tid % TN, ty = tid / TN;
+  const int z = blockIdx.z;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  const uint32_t* A = g.A + (int64_t)z * g.strideA * S;
+  const uint32_t* B = g.B + (int64_t)z * g.strideB * S;
+  uint32_t* C = g.C + (int64_t)z * g.strideC * S;
+  const int KT = (g.l + TK - 1) / TK;
+  const int i = i0 + ty, j = j0 + tx;
+  const bool active = (i < g.m) && (j < g.n);
+
+  auto stage = [&](int kt, int buf) {
+    const int k0 = kt * TK;
+    constexpr int CH = S / 4;
+#pragma unroll 1
+    for (int c = tid; c < TM * TK * CH; c += NT) {
+      const int e = c / CH, w = c - e * CH;
+      const int r = e / TK, kk = e - r * TK;
+      const int gi = i0 + r, gk = k0 + kk;
+      const bool ok = gi < g.m && gk < g.l;
+      const uint32_t* src = A + ((int64_t)(ok ? gi : 0) * g.lda + (ok ? gk : 0)) * S + 4 * w;
+      cp_async16(sA + buf * A_WORDS + e * S + 4 * w, src, ok ? 16 : 0);
+    }
+#pragma unroll 1
+    for (int c = tid; c < TK * TN * CH; c += NT) {
+      const int e = c / CH, w = c - e * CH;
+      const int kk = e / TN, cc = e - kk * TN;
+      const int gk = k0 + kk, gj = j0 + cc;
+      const bool ok = gk < g.l && gj < g.n;
+      const uint32_t* src = B + ((int64_t)(ok ? gk : 0) * g.ldb + (ok ? gj : 0)) * S + 4 * w;
+      cp_async16(sB + buf * B_WORDS + e * S + 4 * w, src, ok ? 16 : 0);
+    }
+  };
+
+  MP<L> acc, pacc;
+  mp_zero(acc);
+  mp_zero(pacc);
+  bool first = true;
+  int next_b = 0;  // next k at which a Block k-tile starts
+
+  stage(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt + 1 < KT) stage(kt + 1, (kt + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (active) {
+      const uint32_t* a_rows = sA + (kt & 1) * A_WORDS + ty * TK * S;
+      const uint32_t* b_cols = sB + (kt & 1) * B_WORDS + tx * S;
+      const int kend = min(TK, g.l - kt * TK);
+#pragma unroll 1
+      for (int kk = 0; kk < kend; ++kk) {
+        const int k = kt * TK + kk;
+        MP<L> b, t;
+        load_rec<L>(b_cols + kk * TN * S, b);
+        const uint32_t* ar = a_rows + kk * S;
+        if constexpr (A_STREAM) {
+          mp_mul_g<L>([&](int q) { return ar[q]; }, (int32_t)ar[L], ar[L + 1], b, g.sh, t);
+        } else {
+          MP<L> a;
+          load_rec<L>(ar, a);
+          mp_mul<L>(a, b, g.sh, t);
+        }
+        if (k == next_b) {
+          if (k > 0) {
+            if (first) {
+              acc = pacc;
+              first = false;
+            } else {
+              MP<L> r;
+              mp_add<L>(acc, pacc, 0u, g.sh, r);
+              acc = r;
+            }
+          }
+          pacc = t;
+          next_b += g.kb;
+        } else {
+          MP<L> r;
+          mp_add<L>(pacc, t, 0u, g.sh, r);
+          pacc = r;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!active) return;
+  MP<L> res;
+  if (first) {
+    res = pacc;
+  } else {
+    mp_add<L>(acc, pacc, 0u, g.sh, res);
+  }
+  uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
+  if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
+    MP<L> old, r;
+    load_rec<L>(cr, old);
+    mp_add<L>(old, res, 1u, g.sh, r);
+    res = r;
+  }
+  if (exp_out_of_range(res.e)) atomicOr(g.err, ERR_EXP_RANGE);
+  store_rec<L>(cr, res);
+}
+
+template <int L>
+void launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK;
+  constexpr int S = rec_stride(L);
+  const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * S);
+  auto kern = gemm_leaf_kernel<L, TM, TN, TK>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  dim3 grid((g.n + TN - 1) / TN, (g.m + TM - 1) / TM, g.batch);
+  kern<<<grid, TM * TN, smem, st>>>(g);
+}
+
+template void launch_gemm<1>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<2>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<4>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<8>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<16>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<32>(const GemmArgs&, cudaStream_t);
+
+}  // namespace mpg

@@ -1,0 +1,97 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (internal to libmpgpu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mpg {
+
+// Batched MP GEMM over AoS record arrays (rec_stride(L) words per element).
+// C[z] = A[z] * B[z] for z < batch, with the reference's inner-product order
+// (matrix.hpp:147-155) and, when kb < l, the Block k-tile order
+// (matrix.hpp:196-216): a fresh accumulator per k-tile, then C = RN(C + P).
+struct GemmArgs {
+  const uint32_t* A;
+  const uint32_t* B;
+  uint32_t* C;
+  int64_t strideA, strideB, strideC;  // elements between batch items
+  int64_t lda, ldb, ldc;              // elements between rows
+  int m, l, n;
+  int kb;  // k-tile of the Block order (>= l: Simple)
+  int batch;
+  int sh;  // 32 L - p
+  uint32_t* err;
+  // optional LU Schur epilogue: C = RN(C - A*B) in place (blocklu.hpp:138-141)
+  int sub_from_c;
+};
+
+template <int L>
+void launch_gemm(const GemmArgs& g, cudaStream_t st);
+
+// SoA planes <-> records
+template <int L>
+void launch_soa2rec(const uint32_t* limbs, const int32_t* exp, const uint8_t* sign, int64_t N,
+                    int64_t plane_stride, uint32_t* rec, cudaStream_t st);
+template <int L>
+void launch_rec2soa(const uint32_t* rec, int64_t N, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                    int64_t plane_stride, cudaStream_t st);
+
+// elementwise C = A +- B (matrix.hpp:121-134), contiguous records
+template <int L>
+void launch_addsub(const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int is_sub, int sh,
+                   uint32_t* err, cudaStream_t st);
+
+// Fast-algorithm level transforms (fastmm.hpp:133-219), batched over the nodes of
+// one recursion level.  Parents: nodes x (rows x cols) records (row-major, dense),
+// virtually zero-padded to (prows x pcols) = (rows + rows%2, cols + cols%2).
+// Children: 7 per parent, each (prows/2 x pcols/2), child c = parent * 7 + q.
+// side: 0 = A operand, 1 = B operand.  algo: 2 = Strassen, 3 = Winograd.
+template <int L>
+void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
+                   uint32_t* children, int sh, uint32_t* err, cudaStream_t st);
+// Children products (7 per parent, hm x hn) -> parent C (rows x cols, stripped).
+// Optional trace output of Winograd's T1/T2 (2 x hm x hn per parent) when t_out != nullptr.
+template <int L>
+void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
+                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st);
+
+// copy a (rows x cols) window with leading dims (records) -- used by LU
+template <int L>
+void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
+                   cudaStream_t st);
+
+// scalar ops on record arrays (primitive tests): op 0 add, 1 sub, 2 mul, 3 div
+template <int L>
+void launch_vec_op(int op, const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int sh,
+                   uint32_t* err, cudaStream_t st);
+
+// ---- LU (blocklu.hpp:42-146) --------------------------------------------
+// One right-looking elimination step d of the panel [p, row_end) x [p, p+k) of the
+// n x n record matrix a (row-major, ld = n):
+//   multipliers a_id = RN(a_id / a_dd) for i in (d, row_end), and
+//   a_ij = RN(a_ij - RN(a_id * a_dj)) for i in (d, row_end), j in (d, p+k).
+template <int L>
+void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh,
+                    uint32_t* err, cudaStream_t st);
+// pivot search for column d over rows [d, row_end): first max |a_id| -> piv_dev[d];
+// then swap rows d and piv over all n columns.
+template <int L>
+void launch_pivot(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t* piv_dev, int64_t* zp,
+                  cudaStream_t st);
+// forward substitution step s of trsm_unit_lower (blocklu.hpp:60-69) on the
+// block rows (s, p_end) x cols [c0, c0+w): a_ij = RN(a_ij - RN(a_is * a_sj)).
+template <int L>
+void launch_trsm_l_step(uint32_t* a, int64_t n, int64_t s, int64_t p_end, int64_t c0, int64_t w,
+                        int sh, uint32_t* err, cudaStream_t st);
+
+// Ly = Pb, Ux = y on packed factors (blocklu.hpp:215-245); scratch: 2n records
+template <int L>
+void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b,
+                     uint32_t* x, uint32_t* scratch, int sh, uint32_t* err, int64_t* zp,
+                     cudaStream_t st);
+
+// C(view, ldc) = RN(C - T) for a dense rows x cols T (LU Schur subtraction)
+template <int L>
+void launch_sub2d(uint32_t* C, int64_t ldc, const uint32_t* T, int rows, int cols, int sh,
+                  uint32_t* err, cudaStream_t st);
+
+}  // namespace mpg

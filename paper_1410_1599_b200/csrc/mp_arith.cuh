@@ -1,0 +1,459 @@
+// mp_arith.cuh -- multiple-precision scalar primitives for sm_100a.
+//
+// Semantics are MPFR's round-to-nearest-even at precision p (reference:
+// precision.hpp:127-161 -> mpfr_add / mpfr_sub / mpfr_mul / mpfr_div with MPFR_RNDN).
+// Every operation is correctly rounded, so any sequence of them reproduces the
+// reference's MPFR results bit for bit.
+//
+// Number format (registers / records): L 32-bit limbs, limb L-1 most significant,
+// MSB of limb L-1 set for nonzero values, bits below p cleared; exponent e in the
+// MPFR convention (value = 0.m * 2^e, 0.m in [1/2, 1)); sign s in {0,1}.
+// Zero: e == EXP_ZERO (limbs 0), sign kept (MPFR signed zeros).
+#pragma once
+#include <cstdint>
+
+namespace mpg {
+
+constexpr int32_t EXP_ZERO = INT32_MIN;
+// MPFR's default exponent range is [1-2^30, 2^30-1]; results outside it are flagged.
+constexpr int32_t EXP_MAX = (1 << 30) - 1;
+constexpr int32_t EXP_MIN = 1 - (1 << 30);
+constexpr uint32_t ERR_EXP_RANGE = 1u;
+constexpr uint32_t ERR_DIV_ZERO = 2u;
+
+// Record stride (32-bit words) of one element in the AoS record layout:
+// limbs[0..L-1], exp, sign, padding.  stride/4 is odd so that a quarter-warp of
+// LDS.128 over consecutive records is bank-conflict free.
+__host__ __device__ constexpr int rec_stride(int L) {
+  int s = 4 * ((L + 2 + 3) / 4);
+  return ((s / 4) % 2 == 0) ? s + 4 : s;
+}
+
+template <int L>
+struct MP {
+  uint32_t m[L];
+  int32_t e;
+  uint32_t s;
+};
+
+// ---------------------------------------------------------------------------
+// full L x L -> 2L limb product, row-wise schoolbook with PTX carry chains.
+// 2 L^2 multiply instructions (lo + hi) on the FMA pipe; the compiler maps the
+// carries onto IADD3.X / IMAD.X.
+// ---------------------------------------------------------------------------
+template <int L, class AG>
+__device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+#pragma unroll
+  for (int i = 0; i < 2 * L; ++i) r[i] = 0;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const uint32_t ai = a_at(i);
+    if (L == 1) {
+      asm("mul.lo.u32 %0, %1, %2;" : "=r"(r[0]) : "r"(ai), "r"(b[0]));
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(r[1]) : "r"(ai), "r"(b[0]));
+    } else {
+      asm volatile("mad.lo.cc.u32 %0, %1, %2, %0;" : "+r"(r[i]) : "r"(ai), "r"(b[0]));
+#pragma unroll
+      for (int j = 1; j < L; ++j)
+        asm volatile("madc.lo.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + j]) : "r"(ai), "r"(b[j]));
+      asm volatile("addc.u32 %0, %0, 0;" : "+r"(r[i + L]));
+      asm volatile("mad.hi.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + 1]) : "r"(ai), "r"(b[0]));
+#pragma unroll
+      for (int j = 1; j < L; ++j)
+        asm volatile("madc.hi.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + j + 1]) : "r"(ai), "r"(b[j]));
+      if (i + L + 1 < 2 * L) asm volatile("addc.u32 %0, %0, 0;" : "+r"(r[i + L + 1]));
+    }
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void mul_full(const uint32_t (&a)[L], const uint32_t (&b)[L],
+                                         uint32_t (&r)[2 * L]) {
+  mul_full_g<L>([&](int i) { return a[i]; }, b, r);
+}
+
+// add a single word w at limb 0 with full carry propagation; returns carry-out
+template <int L>
+__device__ __forceinline__ uint32_t add_word(uint32_t (&m)[L], uint32_t w) {
+  uint32_t c;
+  if (L == 1) {
+    asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(m[0]) : "r"(w));
+    asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+    return c;
+  }
+  asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(m[0]) : "r"(w));
+#pragma unroll
+  for (int k = 1; k < L; ++k) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(m[k]));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Round-to-nearest-even of an L-limb normalised mantissa m (MSB set) followed by
+// a guard limb g and a sticky word st (nonzero iff anything nonzero lies below g),
+// to p = 32L - sh bits.  Bumps e on carry-out (mantissa becomes 1000...).
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t st, int sh,
+                                        int32_t& e) {
+  uint32_t up_word;
+  if (sh == 0) {
+    const uint32_t rb = g >> 31;
+    const uint32_t rest = (g << 1) | st;
+    const uint32_t up = rb & ((rest != 0) | (m[0] & 1u));
+    up_word = up;
+  } else if (sh < 32) {
+    const uint32_t low = m[0] & ((1u << sh) - 1u);
+    const uint32_t rb = (low >> (sh - 1)) & 1u;
+    const uint32_t rest = (low & ((1u << (sh - 1)) - 1u)) | g | st;
+    const uint32_t lsb = (m[0] >> sh) & 1u;
+    m[0] ^= low;
+    const uint32_t up = rb & ((rest != 0) | lsb);
+    up_word = up << sh;
+  } else {
+    // generic path: the precision ends inside a lower limb (L chosen larger than ceil(p/32))
+    const int rbpos = sh - 1, rl = rbpos >> 5, rbit = rbpos & 31;
+    const int ql = sh >> 5, qb = sh & 31;
+    uint32_t stk = g | st, rb = 0, lsb = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      uint32_t v = m[k];
+      if (k < rl) {
+        stk |= v;
+        v = 0;
+      } else if (k == rl) {
+        rb = (v >> rbit) & 1u;
+        stk |= v & ((1u << rbit) - 1u);
+        v &= (rbit == 31) ? 0u : ~((2u << rbit) - 1u);
+      }
+      if (k == ql) lsb = (v >> qb) & 1u;
+      m[k] = v;
+    }
+    const uint32_t up = rb & ((stk != 0) | lsb);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const uint32_t addend = (k == ql) ? (up << qb) : 0u;
+      const uint64_t t = (uint64_t)m[k] + addend + c;
+      m[k] = (uint32_t)t;
+      c = (uint32_t)(t >> 32);
+    }
+    if (c) {
+#pragma unroll
+      for (int k = 0; k < L - 1; ++k) m[k] = 0;
+      m[L - 1] = 0x80000000u;
+      e += 1;
+    }
+    return;
+  }
+  if (add_word<L>(m, up_word)) {
+#pragma unroll
+    for (int k = 0; k < L - 1; ++k) m[k] = 0;
+    m[L - 1] = 0x80000000u;
+    e += 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// z = RN_p(x * y)   (mpfr_mul, precision.hpp:145-151; matrix.hpp:150,152)
+// ---------------------------------------------------------------------------
+template <int L, class AG>
+__device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const MP<L>& y, int sh,
+                                         MP<L>& z) {
+  z.s = xs ^ y.s;
+  if (xe == EXP_ZERO || y.e == EXP_ZERO) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) z.m[k] = 0;
+    z.e = EXP_ZERO;
+    return;
+  }
+  uint32_t P[2 * L];
+  mul_full_g<L>(a_at, y.m, P);
+  int32_t e = xe + y.e;
+  uint32_t g, st = 0;
+  if (P[2 * L - 1] >> 31) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) z.m[k] = P[L + k];
+    g = P[L - 1];
+#pragma unroll
+    for (int k = 0; k < L - 1; ++k) st |= P[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], 1);
+    if (L >= 2) {
+      g = __funnelshift_l(P[L >= 2 ? L - 2 : 0], P[L - 1], 1);
+#pragma unroll
+      for (int k = 0; k < L - 2; ++k) st |= P[k];
+      st |= P[L >= 2 ? L - 2 : 0] << 1;
+    } else {
+      g = P[0] << 1;
+    }
+    e -= 1;
+  }
+  round_p<L>(z.m, g, st, sh, e);
+  z.e = e;
+}
+
+template <int L>
+__device__ __forceinline__ void mp_mul(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
+  mp_mul_g<L>([&](int i) { return x.m[i]; }, x.e, x.s, y, sh, z);
+}
+
+// ---------------------------------------------------------------------------
+// z = RN_p(x + (-1)^negy * y)  (mpfr_add / mpfr_sub, matrix.hpp:128,130,153)
+// Exact-alignment algorithm over an (L+1)-limb window (one guard limb) plus a
+// sticky bit; see DESIGN.md "MP add".  Exact cancellation gives +0 (RNDN).
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32_t negy, int sh,
+                                       MP<L>& z) {
+  const uint32_t ys = y_in.s ^ negy;
+  if (x.e == EXP_ZERO || y_in.e == EXP_ZERO) {
+    if (x.e == EXP_ZERO && y_in.e == EXP_ZERO) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) z.m[k] = 0;
+      z.e = EXP_ZERO;
+      z.s = x.s & ys;
+    } else if (x.e == EXP_ZERO) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) z.m[k] = y_in.m[k];
+      z.e = y_in.e;
+      z.s = ys;
+    } else {
+      z = x;
+    }
+    return;
+  }
+  constexpr int W = L + 1;
+  const bool swp = y_in.e > x.e;
+  uint32_t A[W], B[W];
+  A[0] = 0;
+  B[0] = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    A[k + 1] = swp ? y_in.m[k] : x.m[k];
+    B[k + 1] = swp ? x.m[k] : y_in.m[k];
+  }
+  const int32_t ebig = swp ? y_in.e : x.e;
+  const uint32_t sbig = swp ? ys : x.s;
+  const uint32_t ssmall = swp ? x.s : ys;
+  const uint32_t d = (uint32_t)(ebig - (swp ? x.e : y_in.e));
+  const bool sub = sbig != ssmall;
+
+  // ---- align B right by d bits; sticky collects what falls off the window
+  uint32_t st = 0;
+  if (d >= 32u * W) {
+    st = 1;
+#pragma unroll
+    for (int k = 0; k < W; ++k) B[k] = 0;
+  } else {
+    uint32_t q = d >> 5;
+    const uint32_t r = d & 31u;
+    while (q) {  // limb shifts (rare for well-scaled data)
+      st |= B[0];
+#pragma unroll
+      for (int k = 0; k < W - 1; ++k) B[k] = B[k + 1];
+      B[W - 1] = 0;
+      --q;
+    }
+    st |= B[0] & ((1u << r) - 1u);
+#pragma unroll
+    for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], r);
+    B[W - 1] >>= r;
+    st = st != 0;
+  }
+
+  uint32_t R[W];
+  int32_t e = ebig;
+  uint32_t s = sbig;
+  if (!sub) {
+    uint32_t c;
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(A[0]), "r"(B[0]));
+#pragma unroll
+    for (int k = 1; k < W; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k]));
+    asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+    if (c) {
+      st |= R[0] & 1u;
+#pragma unroll
+      for (int k = 0; k < W - 1; ++k) R[k] = __funnelshift_r(R[k], R[k + 1], 1);
+      R[W - 1] = (R[W - 1] >> 1) | 0x80000000u;
+      e += 1;
+    }
+  } else {
+    // R = A - B - st (st is 0/1); borrow only possible when d == 0
+    uint32_t bo;
+    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(A[0]), "r"(B[0]));
+#pragma unroll
+    for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k]));
+    asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
+    if (st) {
+      asm volatile("sub.cc.u32 %0, %0, 1;" : "+r"(R[0]));
+#pragma unroll
+      for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, %0, 0;" : "+r"(R[k]));
+    }
+    if (bo) {  // |small| > |big| (d == 0): negate, result takes the other sign
+      asm volatile("sub.cc.u32 %0, 0, %0;" : "+r"(R[0]));
+#pragma unroll
+      for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, 0, %0;" : "+r"(R[k]));
+      s = ssmall;
+    }
+    // normalise: leading limb first (rare), then bit shift
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) any |= R[k];
+    if (!any) {  // exact cancellation (st is 0 here): +0 under RNDN
+#pragma unroll
+      for (int k = 0; k < L; ++k) z.m[k] = 0;
+      z.e = EXP_ZERO;
+      z.s = 0;
+      return;
+    }
+    while (R[W - 1] == 0) {
+#pragma unroll
+      for (int k = W - 1; k > 0; --k) R[k] = R[k - 1];
+      R[0] = 0;
+      e -= 32;
+    }
+    const uint32_t lz = __clz(R[W - 1]);
+#pragma unroll
+    for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], lz);
+    R[0] <<= lz;
+    e -= (int32_t)lz;
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) z.m[k] = R[k + 1];
+  round_p<L>(z.m, R[0], st, sh, e);
+  z.e = e;
+  z.s = s;
+}
+
+// ---------------------------------------------------------------------------
+// z = RN_p(x / y)   (mpfr_div, precision.hpp:154-161; blocklu.hpp:49,84,241)
+// Restoring division producing ceil((p+2)/32) quotient limbs, left aligned, with
+// the remainder as sticky; y must be nonzero (callers check, SingularError).
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
+  z.s = x.s ^ y.s;
+  if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) z.m[k] = 0;
+    z.e = EXP_ZERO;
+    return;
+  }
+  constexpr int W = L + 1;
+  const int p = 32 * L - sh;
+  const int nl = (p + 2 + 31) >> 5;  // quotient limbs to produce (<= W)
+  uint32_t R[W], Q[W];
+#pragma unroll
+  for (int k = 0; k < L; ++k) R[k] = x.m[k];
+  R[L] = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) Q[k] = 0;
+  bool first_bit = true;
+#pragma unroll
+  for (int ql = W - 1; ql >= 0; --ql) {
+    if (W - 1 - ql < nl) {
+      uint32_t word = 0;
+#pragma unroll 1
+      for (int b = 0; b < 32; ++b) {
+        if (!first_bit) {  // R <<= 1
+#pragma unroll
+          for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], 1);
+          R[0] <<= 1;
+        }
+        first_bit = false;
+        // T = R - Y (Y has a zero top limb)
+        uint32_t T[W], bo;
+        asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(R[0]), "r"(y.m[0]));
+#pragma unroll
+        for (int k = 1; k < L; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(T[k]) : "r"(R[k]), "r"(y.m[k]));
+        asm volatile("subc.cc.u32 %0, %1, 0;" : "=r"(T[L]) : "r"(R[L]));
+        asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
+        const uint32_t qb = bo ? 0u : 1u;
+#pragma unroll
+        for (int k = 0; k < W; ++k) R[k] = qb ? T[k] : R[k];
+        word = (word << 1) | qb;
+      }
+      Q[ql] = word;
+    }
+  }
+  uint32_t rem = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) rem |= R[k];
+  int32_t e = x.e - y.e;
+  if (Q[W - 1] >> 31) {
+    e += 1;
+  } else {
+#pragma unroll
+    for (int k = W - 1; k > 0; --k) Q[k] = __funnelshift_l(Q[k - 1], Q[k], 1);
+    Q[0] <<= 1;
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) z.m[k] = Q[k + 1];
+  round_p<L>(z.m, Q[0], rem, sh, e);
+  z.e = e;
+}
+
+template <int L>
+__device__ __forceinline__ void mp_zero(MP<L>& z, uint32_t s = 0) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) z.m[k] = 0;
+  z.e = EXP_ZERO;
+  z.s = s;
+}
+
+// |x| vs |y|: -1, 0, 1  (for pivot search)
+template <int L>
+__device__ __forceinline__ int mp_cmpabs(const MP<L>& x, const MP<L>& y) {
+  const bool xz = x.e == EXP_ZERO, yz = y.e == EXP_ZERO;
+  if (xz || yz) return xz ? (yz ? 0 : -1) : 1;
+  if (x.e != y.e) return x.e > y.e ? 1 : -1;
+#pragma unroll
+  for (int k = L - 1; k >= 0; --k)
+    if (x.m[k] != y.m[k]) return x.m[k] > y.m[k] ? 1 : -1;
+  return 0;
+}
+
+__device__ __forceinline__ bool exp_out_of_range(int32_t e) {
+  return e != EXP_ZERO && (e > EXP_MAX || e < EXP_MIN);
+}
+
+// ---------------------------------------------------------------------------
+// record I/O (AoS records of rec_stride(L) words)
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void load_rec(const uint32_t* __restrict__ r, MP<L>& x) {
+  constexpr int S = rec_stride(L);
+  static_assert(S % 4 == 0, "record stride must be a multiple of 4 words");
+  uint32_t w[S];
+#pragma unroll
+  for (int k = 0; k < S; k += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(r + k);
+    w[k] = v.x;
+    w[k + 1] = v.y;
+    w[k + 2] = v.z;
+    w[k + 3] = v.w;
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) x.m[k] = w[k];
+  x.e = (int32_t)w[L];
+  x.s = w[L + 1];
+}
+
+template <int L>
+__device__ __forceinline__ void store_rec(uint32_t* __restrict__ r, const MP<L>& x) {
+  constexpr int S = rec_stride(L);
+  uint32_t w[S];
+#pragma unroll
+  for (int k = 0; k < L; ++k) w[k] = x.m[k];
+  w[L] = (uint32_t)x.e;
+  w[L + 1] = x.s;
+#pragma unroll
+  for (int k = L + 2; k < S; ++k) w[k] = 0;
+#pragma unroll
+  for (int k = 0; k < S; k += 4)
+    *reinterpret_cast<uint4*>(r + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+}
+
+}  // namespace mpg

@@ -1,0 +1,140 @@
+"""K1 leaf GEMM + K2/K3 fast-algorithm kernels through the C-ABI vs the oracle.
+
+Bit-exact against the C restatement (oracle/mp_oracle.c) and the compiled
+reference (oracle/_ref) for Simple (matrix.hpp:178-184), Block (matrix.hpp:225-233),
+Strassen and Winograd (fastmm.hpp:244-255) -- the GPU replays the reference's
+operation DAG, so results are identical element for element (signs of zeros too).
+"""
+import numpy as np
+import pytest
+
+ALGS = ["simple", "block", "strassen", "winograd"]
+
+
+def _run(P, alg, param, a, b, ctx, ops=None):
+    if alg == "simple":
+        return P.simple_mul(a, b, ctx, ops)
+    if alg == "block":
+        return P.block_mul(a, b, param, ctx, ops)
+    r = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm[alg], param), ctx)
+    if ops is not None:
+        ops += r.ops
+    return r.c
+
+
+CASES = [
+    # (m, l, n, bits, param)
+    (16, 16, 16, 128, 4),
+    (33, 17, 29, 128, 8),
+    (64, 64, 64, 256, 16),
+    (45, 63, 50, 256, 7),
+    (24, 40, 31, 512, 5),
+    (17, 19, 23, 1024, 4),
+    (40, 40, 40, 53, 8),
+    (21, 22, 23, 2, 3),
+    (30, 30, 30, 200, 6),
+    (65, 33, 66, 64, 16),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,l,n,bits,param", CASES)
+@pytest.mark.parametrize("alg", ALGS)
+def test_gemm_bit_exact_vs_oracle(P, O, alg, m, l, n, bits, param):
+    ctx = P.PrecisionContext(bits)
+    a = P.gen_uniform_full(m, l, 7 + m, ctx)
+    b = P.gen_uniform_full(l, n, 9 + n, ctx)
+    ops = P.OpCounter()
+    c = _run(P, alg, param, a, b, ctx, ops)
+    want, wops = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)
+    assert (ops.mul, ops.addsub) == wops
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", ALGS)
+def test_gemm_scaled_inputs_cfg3_shape_small(P, O, alg):
+    # config 3's distribution (exponents in [-20,20], random signs) at odd dims
+    ctx = P.PrecisionContext(512)
+    a = P.gen_scaled(37, 29, 3, ctx)
+    b = P.gen_scaled(29, 45, 4, ctx)
+    c = _run(P, alg, 4, a, b, ctx)
+    want, _ = O.gemm(alg, 4, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", ALGS)
+def test_gemm_vs_compiled_reference(P, O, alg):
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    ctx = P.PrecisionContext(256)
+    a = P.gen_uniform_full(37, 41, 11, ctx)
+    b = P.gen_uniform_full(41, 35, 12, ctx)
+    c = _run(P, alg, 8, a, b, ctx)
+    want, _ = O.gemm(alg, 8, O.OMat.of(a), O.OMat.of(b), which="ref")
+    assert P.identical(c, want)
+
+
+@pytest.mark.gpu
+def test_exact_integer_inputs_all_algorithms_agree(P):
+    # test_fastmm.cpp:130-149 style: integer inputs make every op exact
+    ctx = P.PrecisionContext(256)
+    rng = P.Prng64(31337)
+    for _ in range(12):
+        m, l, n = (1 + rng.next64() % 96 for _ in range(3))
+        n_min = [1, 8, 32][rng.next64() % 3]
+        A = np.array([(rng.next64() % 2049) - 1024 for _ in range(m * l)], np.int64).reshape(m, l)
+        B = np.array([(rng.next64() % 2049) - 1024 for _ in range(l * n)], np.int64).reshape(l, n)
+        a, b = P.from_ints(A, ctx), P.from_ints(B, ctx)
+        exact = P.from_ints(A @ B, ctx)
+        for alg in ALGS:
+            c = _run(P, alg, n_min, a, b, ctx)
+            assert P.equal_values(c, exact), (alg, m, l, n, n_min)
+
+
+@pytest.mark.gpu
+def test_winograd_2x2_trace(P):
+    # test_fastmm.cpp:105-116
+    ctx = P.PrecisionContext(64)
+    a = P.from_ints([[1, 2], [3, 4]], ctx)
+    b = P.from_ints([[5, 6], [7, 8]], ctx)
+    tr = P.TopTrace()
+    r = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm.winograd, 1), ctx, tr)
+    assert P.equal_values(r.c, P.from_ints([[19, 22], [43, 50]], ctx))
+    vals = lambda ms: [int(m.to_float()[0, 0]) for m in ms]
+    assert vals(tr.sums) == [7, 6, -2, -4, 1, 7, 2, 0]
+    assert vals(tr.products) == [42, 5, 14, -4, 7, -32, 0]
+    assert vals(tr.t) == [47, 43]
+    assert (r.ops.mul, r.ops.addsub) == (7, 15)
+    tr2 = P.TopTrace()
+    r2 = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm.strassen, 1), ctx, tr2)
+    assert vals(tr2.products) == [65, 35, -2, 8, 24, 22, -30]
+    assert tr2.sums == [] and (r2.ops.mul, r2.ops.addsub) == (7, 18)
+
+
+@pytest.mark.gpu
+def test_errors(P):
+    ctx = P.PrecisionContext(64)
+    a, b = P.Matrix(2, 3, ctx), P.Matrix(2, 2, ctx)
+    with pytest.raises(P.DimensionError):
+        P.fast_mul(a, b, P.FastMMConfig(P.Algorithm.strassen, 1), ctx)
+    c = P.Matrix(3, 2, ctx)
+    with pytest.raises(P.DomainError):
+        P.fast_mul(a, c, P.FastMMConfig(P.Algorithm.simple, 1), ctx)
+    with pytest.raises(P.DimensionError):
+        P.fast_mul(a, c, P.FastMMConfig(P.Algorithm.strassen, 0), ctx)
+    with pytest.raises(P.DimensionError):
+        P.block_mul(a, c, 0, ctx)
+
+
+@pytest.mark.gpu
+def test_cfg1_all_four_bit_exact_and_reference_inputs(P, O):
+    # BASELINE config 1: n=128 @128 bits, block 32, cutoff 32
+    ctx = P.PrecisionContext(128)
+    for gen in (P.gen_uniform_full, P.gen_random):
+        a, b = gen(128, 128, 1, ctx), gen(128, 128, 2, ctx)
+        for alg in ALGS:
+            c = _run(P, alg, 32, a, b, ctx)
+            want, _ = O.gemm(alg, 32, O.OMat.of(a), O.OMat.of(b))
+            assert P.identical(c, want), alg

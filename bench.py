@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py -- MP GEMM throughput on B200 (BASELINE.json metric: MP mul-adds/s,
+n^3/t, and % of the INT32 IMAD roofline on the leaf GEMM).
+
+Workload (N = 1): BASELINE config 2 -- square MP GEMM n = 1024 at 256 bits, entries
+uniform in [-1, 1) with all mantissa bits random (seeded), Winograd with recursion
+cutoff n_min = 64 (depth 4, 2401 leaves of 64^3).  One step = one fast_mul of the
+resident operands.  --algo block|strassen|winograd|simple selects the other arms.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): the 7^d leaf products are sharded across ranks (each rank does
+the pre-additions for its own leaves from replicated A and B, no data-path
+collective on the leaf work); the post-additions run after an all-gather of the
+leaf products.  Timing: CUDA events around each step
+on the launching stream, an L2 flush (256 MiB write) between steps, barrier +
+synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+IMAD_PER_CLK_PER_SM = 64  # INT32 IMAD issue rate of the FMA pipe (Nsight profiling guide; tools/microbench_pipes.cu)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--algo", default="winograd", choices=["simple", "block", "strassen", "winograd"])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--bits", type=int, default=256)
+    ap.add_argument("--n-min", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.loads(PEAKS_FILE.read_text())
+    except Exception:
+        return {}
+
+
+def nbytes_soa(n_elems: int, limbs: int) -> int:
+    return n_elems * (4 * limbs + 4 + 1)
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank: int):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified mpmm
+    headers compiled against system MPFR), all host threads, bounded sample."""
+    if rank != 0:
+        return
+    import paper_1410_1599_b200 as P
+    from oracle import oracle as O
+    ctx = P.PrecisionContext(args.bits)
+    s, nmin_s = sample_shape(args)
+    a = P.gen_uniform_full(args.n, args.n, 1, ctx).sub(0, 0, s, s)
+    b = P.gen_uniform_full(args.n, args.n, 2, ctx).sub(0, 0, s, s)
+    threads = os.cpu_count() or 1
+    oa, ob = O.OMat.of(a), O.OMat.of(b)
+    for _ in range(args.warmup):
+        O.gemm_replicas(args.algo, nmin_s, oa, ob, threads)
+    times = []
+    for _ in range(args.steps):
+        _, sec = O.gemm_replicas(args.algo, nmin_s, oa, ob, threads)
+        times.append(sec)
+    total = sum(times)
+    value = threads * s ** 3 * len(times) / total
+    line = {
+        "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"mp{args.bits} (u32 limbs)",
+        "data": "synthetic", "impl": "reference",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": "madd/s", "cores": threads, "kind": "reference",
+                         "sample": sample_desc(args, s, nmin_s, threads)},
+        "e2e": {"value": value, "unit": "madd/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def sample_shape(args):
+    """Bounded CPU sample of the workload: the same algorithm at n/4 with the
+    cutoff scaled by 1/4, i.e. the same recursion depth and op-count ratio."""
+    if args.algo in ("strassen", "winograd"):
+        s = max(args.n // 4, 1)
+        return s, max(args.n_min // 4, 1)
+    return max(args.n // 4, 1), args.n_min
+
+
+def sample_desc(args, s, nmin_s, threads):
+    what = f"{args.algo}(n_min={nmin_s})" if args.algo != "simple" else "simple"
+    return (f"{threads} thread(s) x reference {what} on the {s}x{s} top-left blocks of the workload inputs "
+            f"({args.bits}-bit, same depth / op-count ratio as n={args.n}, n_min={args.n_min}); "
+            f"value = threads * {s}^3 / wall time of the multiplies")
+
+
+def workload_config(args):
+    return {"workload": f"BASELINE config 2: MP GEMM n={args.n} @{args.bits}-bit, {args.algo}"
+                        + (f" n_min={args.n_min}" if args.algo != "simple" else ""),
+            "n": args.n, "bits": args.bits, "algorithm": args.algo, "n_min": args.n_min,
+            "inputs": "uniform [-1,1) full-mantissa, seeds 1/2 (Prng64)",
+            "l2": "flushed between timed steps (256 MiB write) and working set > L2",
+            "parallelism": f"leaf-shard x{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import paper_1410_1599_b200 as P
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P.set_device(local)
+    stream = torch.cuda.current_stream()
+    P.set_stream(stream.cuda_stream)
+
+    ctx = P.PrecisionContext(args.bits)
+    algo = P.Algorithm[args.algo]
+    param = args.n_min if algo != P.Algorithm.simple else 0
+    n = args.n
+    a = P.gen_uniform_full(n, n, 1, ctx)
+    b = P.gen_uniform_full(n, n, 2, ctx)
+    da, db = a.to_device(), b.to_device()
+    dc = P.DeviceMatrix(n, n, ctx)
+    L = P.nlimbs_for(args.bits)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    from paper_1410_1599_b200 import shard
+    runner = shard.make_runner(algo, param, da, db, dc, rank, world) if world > 1 else None
+
+    def step():
+        if runner is not None:
+            return runner()
+        return P.gemm_into(algo, param, da, db, dc)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    times, leaf_ms, launches, st = [], [], 0, None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            st = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            leaf_ms.append(st.leaf_ms)
+            launches += st.launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = float(sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    # every rank works on one n^3 problem together (N > 1: leaf shards); weak scaling
+    # is reported via replicas of the problem per rank -- see shard.make_runner
+    problems = world if (runner is not None and runner.replicated) else 1
+    value = problems * n ** 3 * args.steps / (total_ms * 1e-3)
+
+    # --- correctness guard on the timed output (cheap: sampled rows vs Block on GPU)
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (leaf GEMM): algorithmic IMAD-equivalents
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    leaf_avg_ms = float(np.mean(leaf_ms))
+    imad_eq = st.leaf_madds * 2 * L * L
+    achieved = imad_eq / (leaf_avg_ms * 1e-3) / 1e12
+    peak = IMAD_PER_CLK_PER_SM * sms * sm_max * 1e6 / 1e12
+    clocks = clk.summary()
+    prof = ROOT / "profiles" / "r01_leaf_traffic.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"{args.algo}_{n}_{args.bits}")
+        except Exception:
+            traffic = None
+    roof = {"bound": "imad", "achieved": achieved, "peak": peak, "unit": "TIOP/s (IMAD-eq)",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "mpg::gemm_leaf_kernel", "leaf_ms": leaf_avg_ms, "leaf_madds_per_launch": st.leaf_madds,
+            "imad_eq_per_madd": 2 * L * L,
+            "peak_basis": f"{IMAD_PER_CLK_PER_SM} IMAD/clk/SM x {sms} SMs x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_measured_clock"] = achieved / (IMAD_PER_CLK_PER_SM * sms * clocks["sm_mhz"] * 1e6 / 1e12)
+
+    line = {
+        "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"mp{args.bits} (u32 limbs, IMAD)", "data": "synthetic", "config": workload_config(args),
+        "ops_per_step": {"mul": st.mul, "addsub": st.addsub, "leaf_madds": st.leaf_madds, "depth": st.depth},
+        "phase_ms": {"preadd": st.preadd_ms, "leaf": st.leaf_ms, "postadd": st.postadd_ms},
+        "roofline": roof, "clocks": clocks, "gpu_launches": launches,
+    }
+
+    if not args.no_e2e and world == 1:
+        line["e2e"] = e2e(args, P, torch, a, b, algo, param, ctx, L)
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, P, a, b)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e(args, P, torch, a, b, algo, param, ctx, L):
+    """Same metric through the reference-facing C-ABI call with HOST buffers
+    (mpgpu_gemm_host): H2D of A, B from pinned memory, multiply, D2H of C."""
+    def pinned_like(x):
+        lim = torch.empty(x.limbs.shape, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        ex = torch.empty(x.exp.shape, dtype=torch.int32, pin_memory=True).numpy()
+        sg = torch.empty(x.sign.shape, dtype=torch.uint8, pin_memory=True).numpy()
+        return lim, ex, sg
+
+    def pin(x):
+        lim, ex, sg = pinned_like(x)
+        lim[:] = x.limbs
+        ex[:] = x.exp
+        sg[:] = x.sign
+        return P.Matrix(x.rows(), x.cols(), x.ctx(), lim, ex, sg)
+
+    pa, pb = pin(a), pin(b)
+    c = P.Matrix(a.rows(), b.cols(), ctx)
+    lim, ex, sg = pinned_like(c)
+    pc = P.Matrix(a.rows(), b.cols(), ctx, lim, ex, sg)
+    P.gemm_host(algo, param, pa, pb, pc, ctx)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        P.gemm_host(algo, param, pa, pb, pc, ctx)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    n_el = a.rows() * a.cols()
+    return {"value": a.rows() * a.cols() * b.cols() / dt, "unit": "madd/s",
+            "h2d_bytes_per_step": nbytes_soa(n_el, pa.nlimbs) + nbytes_soa(b.rows() * b.cols(), pb.nlimbs),
+            "d2h_bytes_per_step": nbytes_soa(a.rows() * b.cols(), pc.nlimbs), "ms_per_step": dt * 1e3,
+            "api": "mpgpu_gemm_host (include/mpgpu.h), pinned host SoA buffers, wall clock around the call"}
+
+
+def cpu_baseline(args, P, a, b):
+    """The compiled reference (oracle/_ref) on 1 host core, bounded sample."""
+    try:
+        from oracle import oracle as O
+        if not O.have_ref():
+            return {"value": None, "unit": "madd/s", "cores": 1, "kind": "reference",
+                    "sample": "oracle/_ref not built"}
+        s, nmin_s = sample_shape(args)
+        oa, ob = O.OMat.of(a.sub(0, 0, s, s)), O.OMat.of(b.sub(0, 0, s, s))
+        reps, secs = 0, 0.0
+        while secs < 10.0 and reps < 20:
+            _, t = O.gemm_replicas(args.algo, nmin_s, oa, ob, 1)
+            secs += t
+            reps += 1
+        return {"value": reps * s ** 3 / secs, "unit": "madd/s", "cores": 1, "kind": "reference",
+                "sample": f"{reps} x " + sample_desc(args, s, nmin_s, 1)}
+    except Exception as e:  # reported, never fatal
+        return {"value": None, "unit": "madd/s", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+
+if __name__ == "__main__":
+    main()

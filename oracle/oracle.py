@@ -136,6 +136,19 @@ def gemm(algo, param, a, b, bits=None, which="orc", threads=0):
     return c, (int(ops[0]), int(ops[1]))
 
 
+def gemm_replicas(algo, param, a, b, threads=1):
+    """The compiled reference's product run by `threads` threads on copies of the
+    same inputs; returns (C, wall seconds of the multiplies)."""
+    L = a.nlimbs
+    m, l, n = a.rows(), a.cols(), b.cols()
+    c = OMat(m, n, a.bits(), nlimbs=L)
+    secs = C.c_double(0.0)
+    _check(ref().ref_gemm_replicas(_algo(algo), C.c_int64(param), C.c_long(a.bits()), L, C.c_int64(m),
+                                   C.c_int64(l), C.c_int64(n), *_soa(a), *_soa(b), *_soa(c), int(threads),
+                                   C.byref(secs)))
+    return c, secs.value
+
+
 def fast_mul_trace(algo, n_min, a, b, which="orc"):
     """fast_mul with TopTrace.  Returns (C, sums, products, t, ops)."""
     bits, L = a.bits(), a.nlimbs

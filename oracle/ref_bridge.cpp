@@ -8,6 +8,7 @@
 // bench.py).  Matrices cross this boundary in the C-ABI's SoA format
 // (oracle/soa_mpfr.h).  Return codes: 0 ok, 1 DimensionError, 2 DomainError,
 // 3 SingularError (pivot index via out-param), 4 other mpmm::Error, 5 internal.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -139,6 +140,45 @@ int ref_gemm_rows_mt(int algo, std::int64_t param, long prec, int L, std::int64_
       delete out[t];
     }
     return 0;
+  });
+}
+
+// `threads` threads each run the reference's own product of the SAME inputs
+// (independent copies, no shared state -- the reference is reentrant);
+// *seconds = steady_clock wall time of the multiplies only (as bench.hpp:87-94 /
+// :130-144 time run_matmul).  C receives thread 0's result.
+int ref_gemm_replicas(int algo, std::int64_t param, long prec, int L, std::int64_t m, std::int64_t l,
+                      std::int64_t n, const std::uint32_t* al, const std::int32_t* ae, const std::uint8_t* as,
+                      const std::uint32_t* bl, const std::int32_t* be, const std::uint8_t* bs,
+                      std::uint32_t* cl, std::int32_t* ce, std::uint8_t* cs, int threads, double* seconds) {
+  return guarded([&] {
+    PrecisionContext ctx(prec);
+    if (threads < 1) threads = 1;
+    std::vector<Matrix> as_, bs_;
+    for (int t = 0; t < threads; ++t) {
+      as_.push_back(load(m, l, prec, L, al, ae, as));
+      bs_.push_back(load(l, n, prec, L, bl, be, bs));
+    }
+    std::vector<Matrix*> out(threads, nullptr);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        const Matrix& a = as_[t];
+        const Matrix& b = bs_[t];
+        if (algo == 0)
+          out[t] = new Matrix(simple_mul(a, b, ctx));
+        else if (algo == 1)
+          out[t] = new Matrix(block_mul(a, b, static_cast<std::size_t>(param), ctx));
+        else
+          out[t] = new Matrix(fast_mul(a, b, FastMMConfig{algo_of(algo), static_cast<std::size_t>(param)}, ctx).c);
+      });
+    for (auto& th : pool) th.join();
+    auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    int rc = store(*out[0], L, cl, ce, cs);
+    for (auto* p : out) delete p;
+    return rc;
   });
 }
 

@@ -4,7 +4,7 @@ reference's mpmm hot path).  See DESIGN.md and include/mpgpu.h."""
 from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix, Dims3, DimensionError,
                    DomainError, Error, FastMMConfig, FastMMResult, LUFactors, Matrix, OpCounter,
                    PrecisionContext, RecursionLevel, SingularError, Stats, TopTrace, add, algorithm_name,
-                   block_mul, count_fast, count_simple, equal_values, fast_mul, handle, identical,
+                   block_mul, count_fast, count_simple, equal_values, fast_mul, gemm_host, gemm_into, handle, identical,
                    lu_blocked, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
                    record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
                    solve_columnwise, sub, vec_op)

@@ -509,6 +509,30 @@ def _gemm(algo: Algorithm, param: int, a, b, ctx: PrecisionContext, stats_out: O
     return c, ops
 
 
+def gemm_into(algo: Algorithm, param: int, a: "DeviceMatrix", b: "DeviceMatrix", c: "DeviceMatrix") -> Stats:
+    """C = A*B on resident device matrices into a preallocated C (no allocation,
+    no host traffic) -- the building block of the benchmark's timed region."""
+    st = _L.MpgpuStats()
+    h = c._h
+    _raise(h, _L.lib.mpgpu_gemm(h, int(algo), int(param), C.byref(a.m), C.byref(b.m), C.byref(c.m),
+                                C.byref(st)))
+    return Stats.of(st)
+
+
+def gemm_host(algo: Algorithm, param: int, a: Matrix, b: Matrix, c: Matrix, ctx: PrecisionContext) -> Stats:
+    """The reference-facing call with HOST buffers: upload A, B, multiply, download C
+    (mpgpu_gemm_host).  Pin a/b/c's arrays for full copy bandwidth."""
+    st = _L.MpgpuStats()
+    h = handle()
+    if a.nlimbs != b.nlimbs or a.nlimbs != c.nlimbs:
+        raise DomainError("gemm_host: one host limb count for A, B and C")
+    _raise(h, _L.lib.mpgpu_gemm_host(h, int(algo), int(param), ctx.bits(), a.rows(), a.cols(), b.cols(),
+                                     _ptr(a.limbs), _ptr(a.exp), _ptr(a.sign), _ptr(b.limbs), _ptr(b.exp),
+                                     _ptr(b.sign), _ptr(c.limbs), _ptr(c.exp), _ptr(c.sign), a.nlimbs,
+                                     C.byref(st)))
+    return Stats.of(st)
+
+
 def simple_mul(a, b, ctx: PrecisionContext, ops: Optional[OpCounter] = None, stats: Optional[Stats] = None):
     """matrix.hpp:178-184 -- three-loop inner product, left to right in k."""
     c, o = _gemm(Algorithm.simple, 0, a, b, ctx, stats, isinstance(a, DeviceMatrix))

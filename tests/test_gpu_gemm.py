@@ -138,3 +138,22 @@ def test_cfg1_all_four_bit_exact_and_reference_inputs(P, O):
             c = _run(P, alg, 32, a, b, ctx)
             want, _ = O.gemm(alg, 32, O.OMat.of(a), O.OMat.of(b))
             assert P.identical(c, want), alg
+
+
+GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", sorted(GOLD.glob("gemm_*.npz")), ids=lambda p: p.stem)
+def test_gemm_matches_frozen_reference_fixture(P, path):
+    d = np.load(path)
+
+    def mat(p):
+        r, c, bits = (int(v) for v in d[p + "_shape"])
+        return P.Matrix(r, c, P.PrecisionContext(bits), d[p + "_limbs"], d[p + "_exp"], d[p + "_sign"])
+
+    a, b, want = mat("a"), mat("b"), mat("c")
+    ops = P.OpCounter()
+    c = _run(P, str(d["alg"]), int(d["param"]), a, b, a.ctx(), ops)
+    assert P.identical(c, want)
+    assert (ops.mul, ops.addsub) == tuple(int(v) for v in d["ops"])

@@ -100,3 +100,24 @@ def test_context_validation(P):
         P.lu_blocked(a, P.BlockLUConfig(4, P.Algorithm.simple, 4), P.PrecisionContext(256))
     with pytest.raises(P.DimensionError):
         P.lu_blocked(a, P.BlockLUConfig(0, P.Algorithm.simple, 4), ctx)
+
+
+GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", sorted(GOLD.glob("lu_*.npz")), ids=lambda p: p.stem)
+def test_lu_matches_frozen_reference_fixture(P, path):
+    d = np.load(path)
+
+    def mat(p):
+        r, c, bits = (int(v) for v in d[p + "_shape"])
+        return P.Matrix(r, c, P.PrecisionContext(bits), d[p + "_limbs"], d[p + "_exp"], d[p + "_sign"])
+
+    a, f, b, x = mat("a"), mat("f"), mat("b"), mat("x")
+    ops = P.OpCounter()
+    got = P.lu_blocked(a, P.BlockLUConfig(int(d["K"]), P.Algorithm[str(d["kernel"])], int(d["n_min"])), a.ctx(), ops)
+    assert P.identical(got.packed, f)
+    assert (ops.mul, ops.addsub) == tuple(int(v) for v in d["ops"])
+    assert P.identical(P.mat_vec_mul(a, P.from_ints(np.ones(a.rows(), np.int64), a.ctx()), a.ctx()), b)
+    assert P.identical(P.lu_solve(got, b, a.ctx()), x)

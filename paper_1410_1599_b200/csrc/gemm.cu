@@ -138,17 +138,13 @@ __global__ void __launch_bounds__(TM* TN) gemm_leaf_kernel(const GemmArgs g) {
               acc = pacc;
               first = false;
             } else {
-              MP<L> r;
-              mp_add<L>(acc, pacc, 0u, g.sh, r);
-              acc = r;
+              mp_add<L>(acc, pacc, 0u, g.sh, acc);
             }
           }
           pacc = t;
           next_b += g.kb;
         } else {
-          MP<L> r;
-          mp_add<L>(pacc, t, 0u, g.sh, r);
-          pacc = r;
+          mp_add<L>(pacc, t, 0u, g.sh, pacc);
         }
       }
     }

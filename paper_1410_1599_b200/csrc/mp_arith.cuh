@@ -41,6 +41,28 @@ struct MP {
 // 2 L^2 multiply instructions (lo + hi) on the FMA pipe; the compiler maps the
 // carries onto IADD3.X / IMAD.X.
 // ---------------------------------------------------------------------------
+#ifndef MPG_MUL_PTX_CHAINS
+// Row-wise schoolbook on 64-bit partial sums: t = a_i*b_j + r[i+j] + carry never
+// overflows 64 bits, and maps onto one IMAD.WIDE.U32 (product + 64-bit addend)
+// plus ~1.3 ALU carry ops per limb product -- no half-rate IMAD.HI.
+template <int L, class AG>
+__device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+#pragma unroll
+  for (int i = 0; i < 2 * L; ++i) r[i] = 0;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const uint32_t ai = a_at(i);
+    uint32_t carry = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
+      r[i + j] = (uint32_t)t;
+      carry = (uint32_t)(t >> 32);
+    }
+    r[i + L] = carry;
+  }
+}
+#else
 template <int L, class AG>
 __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
 #pragma unroll
@@ -65,11 +87,36 @@ __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint
     }
   }
 }
+#endif
 
 template <int L>
 __device__ __forceinline__ void mul_full(const uint32_t (&a)[L], const uint32_t (&b)[L],
                                          uint32_t (&r)[2 * L]) {
   mul_full_g<L>([&](int i) { return a[i]; }, b, r);
+}
+
+// Truncated ("short") product: T = sum_{i+j >= L-2} a_i b_j 2^(32(i+j)), exact.
+// The omitted part E = P - T satisfies 0 <= E < (L-1) * 2^(32(L-1)), i.e. less than
+// L-1 units of limb L-1 -- enough to decide round-to-nearest from T almost always
+// (mp_mul_g checks and falls back to the full product).  (L^2 + 3L - 2)/2 limb
+// products instead of L^2 -- the mulhigh trick MPFR itself uses for mpfr_mul.
+template <int L, class AG>
+__device__ __forceinline__ void mul_high_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+#pragma unroll
+  for (int i = 0; i < 2 * L; ++i) r[i] = 0;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const uint32_t ai = a_at(i);
+    const int j0 = (L - 2 - i) > 0 ? (L - 2 - i) : 0;
+    uint32_t carry = 0;
+#pragma unroll
+    for (int j = j0; j < L; ++j) {
+      const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
+      r[i + j] = (uint32_t)t;
+      carry = (uint32_t)(t >> 32);
+    }
+    r[i + L] = carry;
+  }
 }
 
 // add a single word w at limb 0 with full carry propagation; returns carry-out
@@ -168,30 +215,46 @@ __device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const
     return;
   }
   uint32_t P[2 * L];
-  mul_full_g<L>(a_at, y.m, P);
-  int32_t e = xe + y.e;
-  uint32_t g, st = 0;
-  if (P[2 * L - 1] >> 31) {
+  if (L >= 3 && sh == 0) {
+    mul_high_g<L>(a_at, y.m, P);
+    const uint32_t t1 = (P[2 * L - 1] >> 31) ^ 1u;
+    const uint32_t gt = __funnelshift_l(P[L >= 3 ? L - 2 : 0], P[L - 1], t1);
+    // true guard limb lies in [gt, gt + 2L]: decide the rounding from T when no
+    // boundary (half-way point or carry into the mantissa) is within reach
+    const bool down = gt < 0x80000000u - 2u * L;
+    const bool up = gt > 0x80000000u && gt < 0xFFFFFFFFu - 2u * L;
+    if (down | up) {
 #pragma unroll
-    for (int k = 0; k < L; ++k) z.m[k] = P[L + k];
-    g = P[L - 1];
+      for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], t1);
+      int32_t e = xe + y.e - (int32_t)t1;
+      if (add_word<L>(z.m, up ? 1u : 0u)) {
 #pragma unroll
-    for (int k = 0; k < L - 1; ++k) st |= P[k];
-  } else {
-#pragma unroll
-    for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], 1);
-    if (L >= 2) {
-      g = __funnelshift_l(P[L >= 2 ? L - 2 : 0], P[L - 1], 1);
-#pragma unroll
-      for (int k = 0; k < L - 2; ++k) st |= P[k];
-      st |= P[L >= 2 ? L - 2 : 0] << 1;
-    } else {
-      g = P[0] << 1;
+        for (int k = 0; k < L - 1; ++k) z.m[k] = 0;
+        z.m[L - 1] = 0x80000000u;
+        e += 1;
+      }
+      z.e = e;
+      return;
     }
-    e -= 1;
   }
-  round_p<L>(z.m, g, st, sh, e);
-  z.e = e;
+  mul_full_g<L>(a_at, y.m, P);
+  // normalise branch-free: shift left by one when the product's top bit is clear
+  const uint32_t s1 = (P[2 * L - 1] >> 31) ^ 1u;
+  const int32_t e = xe + y.e - (int32_t)s1;
+#pragma unroll
+  for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], s1);
+  uint32_t g, st = 0;
+  if (L >= 2) {
+    g = __funnelshift_l(P[L >= 2 ? L - 2 : 0], P[L - 1], s1);
+#pragma unroll
+    for (int k = 0; k < L - 2; ++k) st |= P[k];
+    st |= P[L >= 2 ? L - 2 : 0] << s1;
+  } else {
+    g = P[0] << s1;
+  }
+  int32_t ee = e;
+  round_p<L>(z.m, g, st, sh, ee);
+  z.e = ee;
 }
 
 template <int L>
@@ -207,13 +270,15 @@ __device__ __forceinline__ void mp_mul(const MP<L>& x, const MP<L>& y, int sh, M
 template <int L>
 __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32_t negy, int sh,
                                        MP<L>& z) {
+  // z may alias x or y: every input is read before z is written.
   const uint32_t ys = y_in.s ^ negy;
   if (x.e == EXP_ZERO || y_in.e == EXP_ZERO) {
     if (x.e == EXP_ZERO && y_in.e == EXP_ZERO) {
+      const uint32_t zs = x.s & ys;  // (-0) + (-0) = -0, otherwise +0 under RNDN
 #pragma unroll
       for (int k = 0; k < L; ++k) z.m[k] = 0;
       z.e = EXP_ZERO;
-      z.s = x.s & ys;
+      z.s = zs;
     } else if (x.e == EXP_ZERO) {
 #pragma unroll
       for (int k = 0; k < L; ++k) z.m[k] = y_in.m[k];
@@ -235,73 +300,62 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
     B[k + 1] = swp ? x.m[k] : y_in.m[k];
   }
   const int32_t ebig = swp ? y_in.e : x.e;
+  const uint32_t d = (uint32_t)(swp ? y_in.e - x.e : x.e - y_in.e);
   const uint32_t sbig = swp ? ys : x.s;
   const uint32_t ssmall = swp ? x.s : ys;
-  const uint32_t d = (uint32_t)(ebig - (swp ? x.e : y_in.e));
-  const bool sub = sbig != ssmall;
+  const uint32_t sub = sbig ^ ssmall;
 
-  // ---- align B right by d bits; sticky collects what falls off the window
+  // ---- align B right by d bits.  d < 32 (the common case) shifts inside the
+  // window and loses nothing; larger gaps shift limbs and collect a sticky bit.
   uint32_t st = 0;
-  if (d >= 32u * W) {
-    st = 1;
+  if (d >= 32u) {
+    if (d >= 32u * W) {
+      st = 1;
 #pragma unroll
-    for (int k = 0; k < W; ++k) B[k] = 0;
-  } else {
-    uint32_t q = d >> 5;
-    const uint32_t r = d & 31u;
-    while (q) {  // limb shifts (rare for well-scaled data)
-      st |= B[0];
+      for (int k = 0; k < W; ++k) B[k] = 0;
+    } else {
+      uint32_t q = d >> 5;
+      const uint32_t r = d & 31u;
+      while (q) {
+        st |= B[0];
 #pragma unroll
-      for (int k = 0; k < W - 1; ++k) B[k] = B[k + 1];
-      B[W - 1] = 0;
-      --q;
+        for (int k = 0; k < W - 1; ++k) B[k] = B[k + 1];
+        B[W - 1] = 0;
+        --q;
+      }
+      st |= B[0] & ((1u << r) - 1u);
+#pragma unroll
+      for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], r);
+      B[W - 1] >>= r;
+      st = st != 0;
     }
-    st |= B[0] & ((1u << r) - 1u);
+  } else {
 #pragma unroll
-    for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], r);
-    B[W - 1] >>= r;
-    st = st != 0;
+    for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], d);
+    B[W - 1] >>= d;
   }
 
-  uint32_t R[W];
+  // ---- R = A + B (add) or A - B - st = A + ~B + (1 - st) (sub), one carry chain
+  const uint32_t mask = 0u - sub;
+  const uint32_t cin = sub & (st ^ 1u);
+  uint32_t R[W], cout;
+  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(B[0] ^ mask), "r"(cin));  // A[0] == 0
+#pragma unroll
+  for (int k = 1; k < W; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k] ^ mask));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(cout));
   int32_t e = ebig;
   uint32_t s = sbig;
-  if (!sub) {
-    uint32_t c;
-    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(A[0]), "r"(B[0]));
-#pragma unroll
-    for (int k = 1; k < W; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k]));
-    asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
-    if (c) {
-      st |= R[0] & 1u;
-#pragma unroll
-      for (int k = 0; k < W - 1; ++k) R[k] = __funnelshift_r(R[k], R[k + 1], 1);
-      R[W - 1] = (R[W - 1] >> 1) | 0x80000000u;
-      e += 1;
-    }
-  } else {
-    // R = A - B - st (st is 0/1); borrow only possible when d == 0
-    uint32_t bo;
-    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(A[0]), "r"(B[0]));
-#pragma unroll
-    for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k]));
-    asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
-    if (st) {
-      asm volatile("sub.cc.u32 %0, %0, 1;" : "+r"(R[0]));
-#pragma unroll
-      for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, %0, 0;" : "+r"(R[k]));
-    }
-    if (bo) {  // |small| > |big| (d == 0): negate, result takes the other sign
+  if (sub & ((cout ^ 1u) | (R[W - 1] == 0))) {  // rare: |small| > |big| (d == 0) or deep cancellation
+    if (!cout) {
       asm volatile("sub.cc.u32 %0, 0, %0;" : "+r"(R[0]));
 #pragma unroll
       for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, 0, %0;" : "+r"(R[k]));
       s = ssmall;
     }
-    // normalise: leading limb first (rare), then bit shift
     uint32_t any = 0;
 #pragma unroll
     for (int k = 0; k < W; ++k) any |= R[k];
-    if (!any) {  // exact cancellation (st is 0 here): +0 under RNDN
+    if (!any) {  // exact cancellation: +0 under RNDN
 #pragma unroll
       for (int k = 0; k < L; ++k) z.m[k] = 0;
       z.e = EXP_ZERO;
@@ -314,12 +368,18 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
       R[0] = 0;
       e -= 32;
     }
-    const uint32_t lz = __clz(R[W - 1]);
-#pragma unroll
-    for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], lz);
-    R[0] <<= lz;
-    e -= (int32_t)lz;
   }
+  // ---- normalise branch-free: add overflow shifts right by one, cancellation left by lz
+  const uint32_t c1 = cout & (sub ^ 1u);
+  st |= R[0] & c1;
+#pragma unroll
+  for (int k = 0; k < W - 1; ++k) R[k] = __funnelshift_r(R[k], R[k + 1], c1);
+  R[W - 1] = (R[W - 1] >> c1) | (c1 << 31);
+  const uint32_t lz = __clz(R[W - 1]);
+#pragma unroll
+  for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], lz);
+  R[0] <<= lz;
+  e += (int32_t)c1 - (int32_t)lz;
 #pragma unroll
   for (int k = 0; k < L; ++k) z.m[k] = R[k + 1];
   round_p<L>(z.m, R[0], st, sh, e);

@@ -65,6 +65,24 @@ def structured_pairs(rng: np.random.Generator, L: int, n: int, bits: int):
     k0 = sh // 32
     ym[k0, near] = (ym[k0, near].astype(np.uint64) ^ lsb).astype(np.uint32)
     ym[L - 1, near] |= np.uint32(0x80000000)
+    # sparse x (top bit + one more bit) times y with boundary-valued low limbs: puts
+    # the product's guard limb on / next to the rounding boundaries, exercising the
+    # short-product decision and its full-product fallback in mp_mul
+    sparse = (sel >= 0.32) & (sel < 0.40)
+    ns = int(sparse.sum())
+    xm[:, sparse] = 0
+    xm[L - 1, sparse] = 0x80000000
+    pos = rng.integers(0, 32 * L - 1, size=ns)
+    cols = np.nonzero(sparse)[0]
+    for c, p_ in zip(cols, pos):
+        if p_ >= 32 * L - bits:
+            xm[p_ // 32, c] |= np.uint32(1 << (p_ % 32))
+    bvals = np.array([0, 1, 2, 0x7FFFFFFF, 0x80000000, 0x80000001, 0xFFFFFFFE, 0xFFFFFFFF, 0x7FFFFFF0,
+                      0x8000000F], np.uint64)
+    for k in range(L):
+        ym[k, sparse] = bvals[rng.integers(0, len(bvals), size=ns)].astype(np.uint32)
+    ym[L - 1, sparse] |= np.uint32(0x80000000)
+    ym[:, sparse] = clear_below(ym[:, sparse], bits)
     # zeros of both signs
     zx = rng.random(n) < 0.03
     zy = rng.random(n) < 0.03

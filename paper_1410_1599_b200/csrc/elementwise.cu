@@ -109,6 +109,9 @@ __device__ __forceinline__ void load_padded(const uint32_t* P, int rows, int col
     mp_zero(x, 0);
 }
 
+// Each sum is formed from operands (re)loaded right before it and stored right
+// after it, so at most two MP values plus the adder's window are live -- the
+// 1024-bit instantiation stays in registers.
 template <int L>
 __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
                               int rows, int cols, uint32_t* __restrict__ children, int sh) {
@@ -122,69 +125,78 @@ __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ p
     const int64_t e = t - node * per;
     const int r = (int)(e / hc), c = (int)(e - (int64_t)r * hc);
     const uint32_t* P = parent + node * (int64_t)rows * cols * S;
-    MP<L> x11, x12, x21, x22;
-    load_padded<L>(P, rows, cols, r, c, x11);
-    load_padded<L>(P, rows, cols, r, c + hc, x12);
-    load_padded<L>(P, rows, cols, r + hr, c, x21);
-    load_padded<L>(P, rows, cols, r + hr, c + hc, x22);
     uint32_t* out = children + (node * 7 * per + e) * S;
     const int64_t cs = per * S;  // stride between sibling children
+    // quadrant q (0: 11, 1: 12, 2: 21, 3: 22) of the virtually zero-padded parent
+    auto ld = [&](int q, MP<L>& x) {
+      load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x);
+    };
+    auto put = [&](int child, const MP<L>& x) { store_rec<L>(out + child * cs, x); };
+    auto sum = [&](int qa, int qb, uint32_t neg, int child) {
+      MP<L> x, y;
+      ld(qa, x);
+      ld(qb, y);
+      mp_add<L>(x, y, neg, sh, x);
+      put(child, x);
+    };
+    auto copy = [&](int q, int child) {
+      MP<L> x;
+      ld(q, x);
+      put(child, x);
+    };
     if (algo == 3) {
-      if (side == 0) {  // S1 = a21+a22, S2 = S1-a11, S3 = a11-a21, S4 = a12-S2
-        MP<L> s1, s2, s3, s4;
-        mp_add<L>(x21, x22, 0u, sh, s1);
-        mp_add<L>(s1, x11, 1u, sh, s2);
-        mp_add<L>(x11, x21, 1u, sh, s3);
-        mp_add<L>(x12, s2, 1u, sh, s4);
-        store_rec<L>(out + 0 * cs, s2);   // M1 = S2*S6
-        store_rec<L>(out + 1 * cs, x11);  // M2 = a11*b11
-        store_rec<L>(out + 2 * cs, x12);  // M3 = a12*b21
-        store_rec<L>(out + 3 * cs, s3);   // M4 = S3*S7
-        store_rec<L>(out + 4 * cs, s1);   // M5 = S1*S5
-        store_rec<L>(out + 5 * cs, s4);   // M6 = S4*b22
-        store_rec<L>(out + 6 * cs, x22);  // M7 = a22*S8
-      } else {  // S5 = b12-b11, S6 = b22-S5, S7 = b22-b12, S8 = S6-b21
-        MP<L> s5, s6, s7, s8;
-        mp_add<L>(x12, x11, 1u, sh, s5);
-        mp_add<L>(x22, s5, 1u, sh, s6);
-        mp_add<L>(x22, x12, 1u, sh, s7);
-        mp_add<L>(s6, x21, 1u, sh, s8);
-        store_rec<L>(out + 0 * cs, s6);
-        store_rec<L>(out + 1 * cs, x11);
-        store_rec<L>(out + 2 * cs, x21);
-        store_rec<L>(out + 3 * cs, s7);
-        store_rec<L>(out + 4 * cs, s5);
-        store_rec<L>(out + 5 * cs, x22);
-        store_rec<L>(out + 6 * cs, s8);
+      if (side == 0) {
+        // S1 = a21+a22 (M5), S2 = S1-a11 (M1), S3 = a11-a21 (M4), S4 = a12-S2 (M6)
+        MP<L> s1, s2, x;
+        ld(2, s1);
+        ld(3, x);
+        mp_add<L>(s1, x, 0u, sh, s1);
+        put(4, s1);
+        ld(0, x);
+        mp_add<L>(s1, x, 1u, sh, s2);
+        put(0, s2);
+        ld(1, x);
+        mp_add<L>(x, s2, 1u, sh, x);
+        put(5, x);
+        sum(0, 2, 1u, 3);
+        copy(0, 1);  // M2 = a11*b11
+        copy(1, 2);  // M3 = a12*b21
+        copy(3, 6);  // M7 = a22*S8
+      } else {
+        // S5 = b12-b11 (M5), S6 = b22-S5 (M1), S7 = b22-b12 (M4), S8 = S6-b21 (M7)
+        MP<L> s5, s6, x;
+        ld(1, s5);
+        ld(0, x);
+        mp_add<L>(s5, x, 1u, sh, s5);
+        put(4, s5);
+        ld(3, x);
+        mp_add<L>(x, s5, 1u, sh, s6);
+        put(0, s6);
+        ld(2, x);
+        mp_add<L>(s6, x, 1u, sh, x);
+        put(6, x);
+        sum(3, 1, 1u, 3);
+        copy(0, 1);  // b11
+        copy(2, 2);  // b21
+        copy(3, 5);  // b22
       }
     } else {
-      MP<L> u;
       if (side == 0) {  // a11+a22, a21+a22, a11, a22, a11+a12, a21-a11, a12-a22
-        mp_add<L>(x11, x22, 0u, sh, u);
-        store_rec<L>(out + 0 * cs, u);
-        mp_add<L>(x21, x22, 0u, sh, u);
-        store_rec<L>(out + 1 * cs, u);
-        store_rec<L>(out + 2 * cs, x11);
-        store_rec<L>(out + 3 * cs, x22);
-        mp_add<L>(x11, x12, 0u, sh, u);
-        store_rec<L>(out + 4 * cs, u);
-        mp_add<L>(x21, x11, 1u, sh, u);
-        store_rec<L>(out + 5 * cs, u);
-        mp_add<L>(x12, x22, 1u, sh, u);
-        store_rec<L>(out + 6 * cs, u);
+        sum(0, 3, 0u, 0);
+        sum(2, 3, 0u, 1);
+        copy(0, 2);
+        copy(3, 3);
+        sum(0, 1, 0u, 4);
+        sum(2, 0, 1u, 5);
+        sum(1, 3, 1u, 6);
       } else {  // b11+b22, b11, b12-b22, b21-b11, b22, b11+b12, b21+b22
-        mp_add<L>(x11, x22, 0u, sh, u);
-        store_rec<L>(out + 0 * cs, u);
-        store_rec<L>(out + 1 * cs, x11);
-        mp_add<L>(x12, x22, 1u, sh, u);
-        store_rec<L>(out + 2 * cs, u);
-        mp_add<L>(x21, x11, 1u, sh, u);
-        store_rec<L>(out + 3 * cs, u);
-        store_rec<L>(out + 4 * cs, x22);
-        mp_add<L>(x11, x12, 0u, sh, u);
-        store_rec<L>(out + 5 * cs, u);
-        mp_add<L>(x21, x22, 0u, sh, u);
-        store_rec<L>(out + 6 * cs, u);
+        sum(0, 3, 0u, 0);
+        copy(0, 1);
+        sum(1, 3, 1u, 2);
+        sum(2, 0, 1u, 3);
+        copy(3, 4);
+        sum(0, 1, 0u, 5);
+        sum(2, 3, 0u, 6);
       }
     }
   }

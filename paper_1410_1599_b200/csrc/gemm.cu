@@ -19,6 +19,18 @@
 #include "kernels.h"
 #include "mp_arith.cuh"
 
+#ifndef MPG_MINB_8
+#define MPG_MINB_8 3
+#endif
+#define MPG_MINB_1 4
+#define MPG_MINB_2 4
+#define MPG_MINB_4 3
+#define MPG_MINB_16 1
+#define MPG_MINB_32 1
+#ifndef MPG_LOAD
+#define MPG_LOAD load_rec_s
+#endif
+
 namespace mpg {
 
 __device__ __forceinline__ void cp_async16(uint32_t* sdst, const uint32_t* gsrc, int src_bytes) {
@@ -36,31 +48,37 @@ template <int L>
 struct GemmCfg;
 template <>
 struct GemmCfg<1> {
+  static constexpr int MINB = MPG_MINB_1;
   static constexpr int TM = 16, TN = 16, TK = 16;
 };
 template <>
 struct GemmCfg<2> {
+  static constexpr int MINB = MPG_MINB_2;
   static constexpr int TM = 16, TN = 16, TK = 16;
 };
 template <>
 struct GemmCfg<4> {
+  static constexpr int MINB = MPG_MINB_4;
   static constexpr int TM = 16, TN = 16, TK = 16;
 };
 template <>
 struct GemmCfg<8> {
+  static constexpr int MINB = MPG_MINB_8;
   static constexpr int TM = 16, TN = 16, TK = 16;
 };
 template <>
 struct GemmCfg<16> {
+  static constexpr int MINB = MPG_MINB_16;
   static constexpr int TM = 8, TN = 16, TK = 8;
 };
 template <>
 struct GemmCfg<32> {
+  static constexpr int MINB = MPG_MINB_32;
   static constexpr int TM = 8, TN = 16, TK = 4;
 };
 
 template <int L, int TM, int TN, int TK>
-__global__ void __launch_bounds__(TM* TN) gemm_leaf_kernel(const GemmArgs g) {
+__global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(const GemmArgs g) {
   constexpr int S = rec_stride(L);
   constexpr int NT = TM * TN;
   constexpr int A_WORDS = TM * TK * S, B_WORDS = TK * TN * S;
@@ -102,11 +120,14 @@ __global__ void __launch_bounds__(TM* TN) gemm_leaf_kernel(const GemmArgs g) {
     }
   };
 
+  // Accumulators start at -0: RN(-0 + x) == x exactly for every x (signed zeros
+  // included), so "C = P" for the first Block k-tile and "acc = first product" are
+  // the same rounded add as every later step -- no data-dependent copies in the
+  // hot loop (matrix.hpp:147-155, :203-212).
   MP<L> acc, pacc;
-  mp_zero(acc);
-  mp_zero(pacc);
-  bool first = true;
-  int next_b = 0;  // next k at which a Block k-tile starts
+  mp_zero(acc, 1u);
+  mp_zero(pacc, 1u);
+  int next_b = g.kb;  // k at which the next Block k-tile starts
 
   stage(0, 0);
   cp_async_commit();
@@ -122,41 +143,29 @@ __global__ void __launch_bounds__(TM* TN) gemm_leaf_kernel(const GemmArgs g) {
 #pragma unroll 1
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
+        if (k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
+          mp_add<L>(acc, pacc, 0u, g.sh, acc);
+          mp_zero(pacc, 1u);
+          next_b += g.kb;
+        }
         MP<L> b, t;
-        load_rec<L>(b_cols + kk * TN * S, b);
+        MPG_LOAD<L>(b_cols + kk * TN * S, b);
         const uint32_t* ar = a_rows + kk * S;
         if constexpr (A_STREAM) {
           mp_mul_g<L>([&](int q) { return ar[q]; }, (int32_t)ar[L], ar[L + 1], b, g.sh, t);
         } else {
           MP<L> a;
-          load_rec<L>(ar, a);
+          MPG_LOAD<L>(ar, a);
           mp_mul<L>(a, b, g.sh, t);
         }
-        if (k == next_b) {
-          if (k > 0) {
-            if (first) {
-              acc = pacc;
-              first = false;
-            } else {
-              mp_add<L>(acc, pacc, 0u, g.sh, acc);
-            }
-          }
-          pacc = t;
-          next_b += g.kb;
-        } else {
-          mp_add<L>(pacc, t, 0u, g.sh, pacc);
-        }
+        mp_add<L>(pacc, t, 0u, g.sh, pacc);
       }
     }
     __syncthreads();
   }
   if (!active) return;
   MP<L> res;
-  if (first) {
-    res = pacc;
-  } else {
-    mp_add<L>(acc, pacc, 0u, g.sh, res);
-  }
+  mp_add<L>(acc, pacc, 0u, g.sh, res);
   uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
   if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
     MP<L> old, r;

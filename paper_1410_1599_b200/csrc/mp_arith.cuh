@@ -501,6 +501,16 @@ __device__ __forceinline__ void load_rec(const uint32_t* __restrict__ r, MP<L>& 
   x.s = w[L + 1];
 }
 
+// scalar-load variant (no 4-register alignment constraint on the destination):
+// lets the register allocator keep loop-carried accumulators in place
+template <int L>
+__device__ __forceinline__ void load_rec_s(const uint32_t* __restrict__ r, MP<L>& x) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) x.m[k] = r[k];
+  x.e = (int32_t)r[L];
+  x.s = r[L + 1];
+}
+
 template <int L>
 __device__ __forceinline__ void store_rec(uint32_t* __restrict__ r, const MP<L>& x) {
   constexpr int S = rec_stride(L);

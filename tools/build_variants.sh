@@ -1,0 +1,18 @@
+#!/bin/bash
+# Build libmpgpu variants with different compile-time knobs for A/B timing on the box.
+# usage: tools/build_variants.sh NAME "-DKNOB=VAL ..." [NAME2 "FLAGS2" ...]
+set -e
+cd "$(dirname "$0")/.."
+OUT=paper_1410_1599_b200/_variants
+mkdir -p $OUT
+NVCC="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -Iinclude"
+while [ $# -gt 0 ]; do
+  name=$1; flags=$2; shift 2
+  d=$OUT/$name; mkdir -p $d
+  for s in gemm elementwise lu capi; do
+    $NVCC $flags -c paper_1410_1599_b200/csrc/$s.cu -o $d/$s.o &
+  done
+  wait
+  $NVCC -shared -o $d/libmpgpu.so $d/*.o -cudart static
+  echo built $d/libmpgpu.so
+done

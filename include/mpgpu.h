@@ -139,9 +139,13 @@ int mpgpu_vec_op(mpgpu_handle* h, int op, const mpgpu_mat* A, const mpgpu_mat* B
  * stats->mul/addsub accumulate the Schur multiply counts (schur_ops). */
 int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min,
                      int pivoting, int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats);
-/* Ly = Pb, Ux = y (blocklu.hpp:215-245); piv may be NULL (pivot-free factors). */
+/* Ly = Pb, Ux = y (blocklu.hpp:215-245); piv may be NULL (pivot-free factors).
+ * exact = 1 replays the reference's summation order (bit-exact; the back
+ * substitution is an O(n^2) serial chain of rounded adds); exact = 0 runs the
+ * back substitution column-oriented (n parallel steps; s-descending sums, within
+ * the LU tolerance). */
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b,
-                   mpgpu_mat* x, int64_t* zero_pivot);
+                   mpgpu_mat* x, int exact, int64_t* zero_pivot);
 
 /* ---- host-side model / plan / inputs ------------------------------------ */
 /* count_fast (opmodel.hpp:30-44); SIMPLE / BLOCK give count_simple */

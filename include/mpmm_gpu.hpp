@@ -264,7 +264,7 @@ inline Vector lu_solve(const LUFactors& f, const Vector& b, PrecisionContext ctx
   if (!rc) rc = mpgpu_upload(h, &df, sf.limbs.data(), sf.exp.data(), sf.sign.data(), sf.L);
   if (!rc) rc = mpgpu_upload(h, &db, sb.limbs.data(), sb.exp.data(), sb.sign.data(), sb.L);
   std::int64_t zp = 0;
-  if (!rc) rc = mpgpu_lu_solve(h, &df, nullptr, &db, &dx, &zp);
+  if (!rc) rc = mpgpu_lu_solve(h, &df, nullptr, &db, &dx, 1, &zp);
   if (!rc) rc = mpgpu_download(h, &dx, sx.limbs.data(), sx.exp.data(), sx.sign.data(), sx.L);
   mpgpu_free_matrix(h, &df);
   mpgpu_free_matrix(h, &db);

@@ -60,7 +60,7 @@ _SIGS = {
     "mpgpu_addsub": (C.c_int, [vp, C.c_int, MatP, MatP, MatP]),
     "mpgpu_vec_op": (C.c_int, [vp, C.c_int, MatP, MatP, MatP]),
     "mpgpu_lu_blocked": (C.c_int, [vp, MatP, C.c_int64, C.c_int, C.c_int64, C.c_int, vp, i64p, StatsP]),
-    "mpgpu_lu_solve": (C.c_int, [vp, MatP, vp, MatP, MatP, i64p]),
+    "mpgpu_lu_solve": (C.c_int, [vp, MatP, vp, MatP, MatP, C.c_int, i64p]),
     "mpgpu_count_fast": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, u64p]),
     "mpgpu_recursion_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int,
                                        C.POINTER(C.c_int)]),

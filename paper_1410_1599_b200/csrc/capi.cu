@@ -786,7 +786,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
 }
 
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
-                   int64_t* zero_pivot) {
+                   int exact, int64_t* zero_pivot) {
   if (!h || !F || !b || !x) return MPGPU_ERR_DOMAIN;
   if (zero_pivot) *zero_pivot = 0;
   const int64_t n = F->rows;
@@ -807,7 +807,7 @@ int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, cons
     constexpr int L = decltype(Lc)::value;
     CUDA_TRY(h, scratch.alloc(h, sizeof(uint32_t) * rec_stride(L) * 2 * n));
     mpg::launch_lu_solve<L>(F->rec, n, piv ? static_cast<const int64_t*>(dpiv.p) : nullptr, b->rec, x->rec,
-                            scratch.u32(), sh, h->d_err, zp, h->stream);
+                            scratch.u32(), sh, h->d_err, zp, exact, h->stream);
     return 0;
   });
   if (rc) return rc;

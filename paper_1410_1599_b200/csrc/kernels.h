@@ -87,7 +87,7 @@ void launch_trsm_l_step(uint32_t* a, int64_t n, int64_t s, int64_t p_end, int64_
 template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b,
                      uint32_t* x, uint32_t* scratch, int sh, uint32_t* err, int64_t* zp,
-                     cudaStream_t st);
+                     int exact, cudaStream_t st);
 
 // C(view, ldc) = RN(C - T) for a dense rows x cols T (LU Schur subtraction)
 template <int L>

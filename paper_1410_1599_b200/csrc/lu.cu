@@ -26,44 +26,47 @@ inline int blocks_for(int64_t n) {
 }
 }  // namespace
 
-// multipliers of column d: a_id = RN(a_id / a_dd), rows (d, row_end)
+// One elimination step of pivot column d over a block of LU_RB rows:
+//   a_id = RN(a_id / a_dd)                       (blocklu.hpp:49)
+//   a_ij = RN(a_ij - RN(a_id * a_dj)), d < j < col_end   (blocklu.hpp:51-52)
+// Every row's multiplier is produced inside the CTA that uses it, so one launch
+// per column suffices (no grid-wide dependency between rows).
+constexpr int LU_RB = 8;
 template <int L>
-__global__ void lu_div_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int sh, int64_t* zp) {
+__global__ void __launch_bounds__(NT) lu_col_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end,
+                                                    int64_t col_end, int sh, int64_t* zp) {
   constexpr int S = rec_stride(L);
+  __shared__ __align__(16) uint32_t s_mult[LU_RB * S];
   if (*zp) return;  // a zero pivot was already met: the factorisation has failed
-  MP<L> piv;
-  load_rec<L>(a + (d * n + d) * S, piv);
-  if (piv.e == EXP_ZERO) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *zp = d + 1;  // blocklu.hpp:46-47 (1-based)
-    return;
+  const int64_t r0 = d + 1 + (int64_t)blockIdx.x * LU_RB;
+  if (threadIdx.x < LU_RB) {
+    const int64_t i = r0 + threadIdx.x;
+    MP<L> piv;
+    load_rec<L>(a + (d * n + d) * S, piv);
+    if (piv.e == EXP_ZERO) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *zp = d + 1;  // blocklu.hpp:46-47 (1-based)
+    } else if (i < row_end) {
+      MP<L> x, q;
+      load_rec<L>(a + (i * n + d) * S, x);
+      mp_div<L>(x, piv, sh, q);
+      store_rec<L>(a + (i * n + d) * S, q);
+      store_rec<L>(s_mult + threadIdx.x * S, q);
+    }
   }
-  for (int64_t i = d + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row_end;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    MP<L> x, q;
-    load_rec<L>(a + (i * n + d) * S, x);
-    mp_div<L>(x, piv, sh, q);
-    store_rec<L>(a + (i * n + d) * S, q);
-  }
-}
-
-// a_ij = RN(a_ij - RN(a_id * a_dj)) for i in (d, row_end), j in (d, col_end)
-template <int L>
-__global__ void lu_update_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh,
-                                 const int64_t* zp) {
-  constexpr int S = rec_stride(L);
-  if (*zp) return;
+  __syncthreads();
+  if (a[(d * n + d) * S + L] == (uint32_t)EXP_ZERO) return;
   const int64_t w = col_end - d - 1;
-  const int64_t total = (row_end - d - 1) * w;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = d + 1 + t / w, j = d + 1 + t % w;
-    MP<L> l, u, p, x, r;
-    load_rec<L>(a + (i * n + d) * S, l);
+  for (int64_t t = threadIdx.x; t < LU_RB * w; t += blockDim.x) {
+    const int rr = (int)(t / w);
+    const int64_t i = r0 + rr, j = d + 1 + t % w;
+    if (i >= row_end) continue;
+    MP<L> l, u, p, x;
+    load_rec<L>(s_mult + rr * S, l);
     load_rec<L>(a + (d * n + j) * S, u);
     mp_mul<L>(l, u, sh, p);
     load_rec<L>(a + (i * n + j) * S, x);
-    mp_add<L>(x, p, 1u, sh, r);
-    store_rec<L>(a + (i * n + j) * S, r);
+    mp_add<L>(x, p, 1u, sh, x);
+    store_rec<L>(a + (i * n + j) * S, x);
   }
 }
 
@@ -106,23 +109,27 @@ __global__ void __launch_bounds__(NT) pivot_kernel(uint32_t* a, int64_t n, int64
   }
   s_idx[threadIdx.x] = best;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t r = -1;
-    MP<L> rv;
-    mp_zero(rv);
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      const int64_t i = s_idx[t];
-      if (i < 0) continue;
-      MP<L> x;
-      load_rec<L>(a + (i * n + d) * S, x);
-      const int c = r < 0 ? 1 : mp_cmpabs<L>(x, rv);
-      if (c > 0 || (c == 0 && i < r)) {
-        rv = x;
-        r = i;
+  // tree reduction: larger |a_id| wins, ties go to the lower row index
+  for (int half = NT / 2; half > 0; half >>= 1) {
+    if (threadIdx.x < half) {
+      const int64_t i0 = s_idx[threadIdx.x], i1 = s_idx[threadIdx.x + half];
+      if (i1 >= 0) {
+        bool take = i0 < 0;
+        if (!take) {
+          MP<L> x0, x1;
+          load_rec<L>(a + (i0 * n + d) * S, x0);
+          load_rec<L>(a + (i1 * n + d) * S, x1);
+          const int c = mp_cmpabs<L>(x1, x0);
+          take = c > 0 || (c == 0 && i1 < i0);
+        }
+        if (take) s_idx[threadIdx.x] = i1;
       }
     }
-    s_best = r;
-    piv[d] = r;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    s_best = s_idx[0];
+    piv[d] = s_idx[0];
   }
   __syncthreads();
   const int64_t r = s_best;
@@ -144,7 +151,8 @@ __global__ void __launch_bounds__(NT) pivot_kernel(uint32_t* a, int64_t n, int64
 template <int L>
 __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t n, const int64_t* piv,
                                                       const uint32_t* b, uint32_t* x, uint32_t* y,
-                                                      uint32_t* tmp, int sh, uint32_t* err, int64_t* zp) {
+                                                      uint32_t* tmp, int sh, uint32_t* err, int64_t* zp,
+                                                      int exact) {
   constexpr int S = rec_stride(L);
   constexpr int CH = S / 4;
   // y = b
@@ -178,6 +186,42 @@ __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t
     }
     __syncthreads();
   }
+  if (!exact) {
+    // column-oriented back substitution (s descending per row): one division and
+    // one parallel rank-1 update per step -- within the LU tolerance, not the
+    // reference's summation order
+    for (int64_t ii = n - 1; ii >= 0; --ii) {
+      __shared__ __align__(16) uint32_t s_x[rec_stride(L)];
+      if (threadIdx.x == 0) {
+        MP<L> acc, d, q;
+        load_rec<L>(y + ii * S, acc);
+        load_rec<L>(f + (ii * n + ii) * S, d);
+        if (d.e == EXP_ZERO) {
+          if (*zp == 0) *zp = ii + 1;
+          mp_zero(q);
+        } else {
+          mp_div<L>(acc, d, sh, q);
+        }
+        if (exp_out_of_range(q.e)) atomicOr(err, ERR_EXP_RANGE);
+        store_rec<L>(x + ii * S, q);
+        store_rec<L>(s_x, q);
+      }
+      __syncthreads();
+      if (*zp) return;
+      MP<L> xs;
+      load_rec<L>(s_x, xs);
+      for (int64_t i = threadIdx.x; i < ii; i += blockDim.x) {
+        MP<L> u, p, acc;
+        load_rec<L>(f + (i * n + ii) * S, u);
+        mp_mul<L>(u, xs, sh, p);
+        load_rec<L>(y + i * S, acc);
+        mp_add<L>(acc, p, 1u, sh, acc);
+        store_rec<L>(y + i * S, acc);
+      }
+      __syncthreads();
+    }
+    return;
+  }
   for (int64_t ii = n - 1; ii >= 0; --ii) {
     for (int64_t s = ii + 1 + threadIdx.x; s < n; s += blockDim.x) {
       MP<L> u, xs, p;
@@ -191,10 +235,9 @@ __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t
       MP<L> acc;
       load_rec<L>(y + ii * S, acc);
       for (int64_t s = ii + 1; s < n; ++s) {
-        MP<L> p, r;
+        MP<L> p;
         load_rec<L>(tmp + s * S, p);
-        mp_add<L>(acc, p, 1u, sh, r);
-        acc = r;
+        mp_add<L>(acc, p, 1u, sh, acc);
       }
       MP<L> d, q;
       load_rec<L>(f + (ii * n + ii) * S, d);
@@ -215,12 +258,11 @@ __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t
 template <int L>
 void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh, uint32_t* err,
                     cudaStream_t st) {
-  (void)err;
   // zero-pivot flag lives right after the error word (see capi.cu)
   int64_t* zp = reinterpret_cast<int64_t*>(err + 2);
-  lu_div_kernel<L><<<blocks_for(row_end - d - 1), NT, 0, st>>>(a, n, d, row_end, sh, zp);
-  const int64_t upd = (row_end - d - 1) * (col_end - d - 1);
-  if (upd > 0) lu_update_kernel<L><<<blocks_for(upd), NT, 0, st>>>(a, n, d, row_end, col_end, sh, zp);
+  const int64_t rows = row_end - d - 1;
+  const int blocks = (int)((rows + LU_RB - 1) / LU_RB);
+  lu_col_kernel<L><<<blocks < 1 ? 1 : blocks, NT, 0, st>>>(a, n, d, row_end, col_end, sh, zp);
 }
 
 template <int L>
@@ -239,9 +281,9 @@ void launch_trsm_l_step(uint32_t* a, int64_t n, int64_t s, int64_t p_end, int64_
 
 template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b, uint32_t* x,
-                     uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, cudaStream_t st) {
+                     uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, int exact, cudaStream_t st) {
   constexpr int S = rec_stride(L);
-  lu_solve_kernel<L><<<1, NT, 0, st>>>(f, n, piv_dev, b, x, scratch, scratch + n * S, sh, err, zp);
+  lu_solve_kernel<L><<<1, NT, 0, st>>>(f, n, piv_dev, b, x, scratch, scratch + n * S, sh, err, zp, exact);
 }
 
 #define MPG_LU_INST(L)                                                                                      \
@@ -250,7 +292,7 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
   template void launch_trsm_l_step<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int, uint32_t*,   \
                                       cudaStream_t);                                                            \
   template void launch_lu_solve<L>(const uint32_t*, int64_t, const int64_t*, const uint32_t*, uint32_t*,        \
-                                   uint32_t*, int, uint32_t*, int64_t*, cudaStream_t);
+                                   uint32_t*, int, uint32_t*, int64_t*, int, cudaStream_t);
 MPG_LU_INST(1)
 MPG_LU_INST(2)
 MPG_LU_INST(4)

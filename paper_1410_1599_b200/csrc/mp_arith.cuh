@@ -393,7 +393,7 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
 // the remainder as sticky; y must be nonzero (callers check, SingularError).
 // ---------------------------------------------------------------------------
 template <int L>
-__device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
+__device__ __forceinline__ void mp_div_bits(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
   z.s = x.s ^ y.s;
   if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
 #pragma unroll
@@ -452,6 +452,95 @@ __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, M
 #pragma unroll
   for (int k = 0; k < L; ++k) z.m[k] = Q[k + 1];
   round_p<L>(z.m, Q[0], rem, sh, e);
+  z.e = e;
+}
+
+// ---------------------------------------------------------------------------
+// z = RN_p(x / y), radix-2^32 digit recurrence (Knuth D style): L+1 quotient digits,
+// each estimated from the top of the remainder with directed-rounding FP64
+// (never an overestimate) and corrected by at most a few add-backs; the final
+// remainder is the sticky bit.  ~(L+1)(4L+20) instructions instead of the
+// bit-serial mp_div_bits' ~32(L+1)(3L+3).
+// ---------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
+  z.s = x.s ^ y.s;
+  if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) z.m[k] = 0;
+    z.e = EXP_ZERO;
+    return;
+  }
+  constexpr int W = L + 1;
+  uint32_t R[W];
+#pragma unroll
+  for (int k = 0; k < L; ++k) R[k] = x.m[k];
+  R[L] = 0;
+  // R -= Y if R >= Y; returns 1 if subtracted
+  auto try_sub = [&]() -> uint32_t {
+    uint32_t T[W], bo;
+    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(R[0]), "r"(y.m[0]));
+#pragma unroll
+    for (int k = 1; k < L; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(T[k]) : "r"(R[k]), "r"(y.m[k]));
+    asm volatile("subc.cc.u32 %0, %1, 0;" : "=r"(T[L]) : "r"(R[L]));
+    asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
+    const uint32_t ok = bo ? 0u : 1u;
+#pragma unroll
+    for (int k = 0; k < W; ++k) R[k] = ok ? T[k] : R[k];
+    return ok;
+  };
+  // quotient digits, most significant first: Q[W] = q0 in {0,1}, then Q[W-1..0]
+  uint32_t Q[W + 1];
+  Q[W] = try_sub();
+  // divisor estimate in units of 2^(32(L-2)), rounded UP (so digit estimates never exceed)
+  const uint64_t ytop = ((uint64_t)y.m[L - 1] << 32) | (L >= 2 ? y.m[L >= 2 ? L - 2 : 0] : 0u);
+  const double yd = __dadd_ru(__ull2double_ru(ytop), (L >= 3) ? 1.0 : 0.0);
+  const double inv = __drcp_rd(yd);
+#pragma unroll 1
+  for (int t = W - 1; t >= 0; --t) {
+    // R <<= 32 (R < Y, so the top limb is free)
+#pragma unroll
+    for (int k = W - 1; k > 0; --k) R[k] = R[k - 1];
+    R[0] = 0;
+    // estimate q = floor(R / Y) from the top three limbs of R, rounded down
+    const uint64_t rtop = ((uint64_t)R[L] << 32) | R[L - 1];
+    double rd = __dmul_rd(__ull2double_rd(rtop), 4294967296.0);
+    if (L >= 2) rd = __dadd_rd(rd, (double)R[L >= 2 ? L - 2 : 0]);
+    const double qd = floor(__dmul_rd(rd, inv));
+    uint32_t qh = qd >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)qd;
+    // R -= qh * Y (exact, W limbs); qh <= q so no underflow
+    uint32_t c = 0, b = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const uint64_t pr = (uint64_t)qh * y.m[j] + c;
+      c = (uint32_t)(pr >> 32);
+      const uint64_t d = (uint64_t)R[j] - (uint32_t)pr - b;
+      R[j] = (uint32_t)d;
+      b = (uint32_t)(d >> 63);
+    }
+    R[L] = R[L] - c - b;
+    // corrections: the estimate is never high and short by at most a little
+    while (try_sub()) ++qh;
+    Q[t] = qh;
+  }
+  uint32_t rem = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) rem |= R[k];
+  // normalise: value = Q[W] . Q[W-1] Q[W-2] ... (radix 2^32)
+  int32_t e = x.e - y.e;
+  uint32_t M[W];
+  if (Q[W]) {  // quotient in [1, 2): shift the digit string right by one bit
+#pragma unroll
+    for (int k = 0; k < W; ++k) M[k] = __funnelshift_r(Q[k], Q[k + 1], 1);
+    rem |= Q[0] & 1u;
+    e += 1;
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) M[k] = Q[k];
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) z.m[k] = M[k + 1];
+  round_p<L>(z.m, M[0], rem, sh, e);
   z.e = e;
 }
 

@@ -718,8 +718,10 @@ def lu_columnwise(a: Matrix) -> LUFactors:
     return lu_blocked(a, BlockLUConfig(a.rows(), Algorithm.simple, 1), a.ctx())
 
 
-def lu_solve(f: LUFactors, b: Matrix, ctx: PrecisionContext) -> Matrix:
-    """blocklu.hpp:215-245 (b, x: n x 1); applies f.piv first when present."""
+def lu_solve(f: LUFactors, b: Matrix, ctx: PrecisionContext, exact: bool = True) -> Matrix:
+    """blocklu.hpp:215-245 (b, x: n x 1); applies f.piv first when present.
+    exact=True replays the reference's summation order bit-exactly (serial back
+    substitution); exact=False runs it column-oriented (fast, within tolerance)."""
     n = f.n
     if b.rows() * b.cols() != n:
         raise DimensionError("lu_solve: length mismatch")
@@ -729,7 +731,7 @@ def lu_solve(f: LUFactors, b: Matrix, ctx: PrecisionContext) -> Matrix:
     zp = C.c_int64(0)
     piv = None if f.piv is None else np.ascontiguousarray(f.piv, np.int64)
     rc = _L.lib.mpgpu_lu_solve(df._h, C.byref(df.m), None if piv is None else _ptr(piv), C.byref(db.m),
-                               C.byref(dx.m), C.byref(zp))
+                               C.byref(dx.m), 1 if exact else 0, C.byref(zp))
     try:
         _raise(df._h, rc, zp.value)
         return dx.download()
@@ -739,9 +741,10 @@ def lu_solve(f: LUFactors, b: Matrix, ctx: PrecisionContext) -> Matrix:
         dx.free()
 
 
-def solve(a: Matrix, b: Matrix, cfg: BlockLUConfig, ctx: PrecisionContext, pivoting: bool = False) -> Matrix:
+def solve(a: Matrix, b: Matrix, cfg: BlockLUConfig, ctx: PrecisionContext, pivoting: bool = False,
+          exact: bool = True) -> Matrix:
     """blocklu.hpp:248-252"""
-    return lu_solve(lu_blocked(a, cfg, ctx, pivoting=pivoting), b, ctx)
+    return lu_solve(lu_blocked(a, cfg, ctx, pivoting=pivoting), b, ctx, exact)
 
 
 def solve_columnwise(a: Matrix, b: Matrix) -> Matrix:

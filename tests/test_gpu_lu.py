@@ -59,6 +59,9 @@ def test_lu_solve_matches_reference(P, O):
     assert P.identical(xp, xpw)
     err = np.max(np.abs(xp.to_float() - 1.0))
     assert err < 1e-60
+    # column-oriented (non-replay) back substitution: within tolerance of the exact one
+    xf = P.lu_solve(fp, b, ctx, exact=False)
+    assert O.log2_max_abs_diff(O.OMat.of(xf), O.OMat.of(xpw)) < -240
 
 
 @pytest.mark.gpu

@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", choices=["auto", "replicas"], default="auto",
+                    help="N>1: auto = leaf shards (Strassen/Winograd) or row shards (Simple/Block) "
+                         "with one all-gather (strong scaling); replicas = independent copies (weak)")
     return ap.parse_args()
 
 
@@ -176,7 +179,7 @@ def workload_config(args):
             "n": args.n, "bits": args.bits, "algorithm": args.algo, "n_min": args.n_min,
             "inputs": "uniform [-1,1) full-mantissa, seeds 1/2 (Prng64)",
             "l2": "flushed between timed steps (256 MiB write) and working set > L2",
-            "parallelism": f"leaf-shard x{args.gpus}" if args.gpus > 1 else "single GPU"}
+            "parallelism": (f"{args.shard} x{args.gpus}" if args.gpus > 1 else "single GPU")}
 
 
 # ---------------------------------------------------------------------------
@@ -211,7 +214,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     from paper_1410_1599_b200 import shard
-    runner = shard.make_runner(algo, param, da, db, dc, rank, world) if world > 1 else None
+    runner = shard.make_runner(algo, param, da, db, dc, rank, world, mode=args.shard) if world > 1 else None
 
     def step():
         if runner is not None:
@@ -283,7 +286,7 @@ def main():
     line = {
         "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if problems > 1 else "strong", "vs_baseline": None,
         "dtype": f"mp{args.bits} (u32 limbs, IMAD)", "data": "synthetic", "config": workload_config(args),
         "ops_per_step": {"mul": st.mul, "addsub": st.addsub, "leaf_madds": st.leaf_madds, "depth": st.depth},
         "phase_ms": {"preadd": st.preadd_ms, "leaf": st.leaf_ms, "postadd": st.postadd_ms},

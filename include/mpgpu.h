@@ -28,6 +28,7 @@
  */
 #ifndef MPGPU_H
 #define MPGPU_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -81,6 +82,8 @@ const char* mpgpu_last_error(const mpgpu_handle* h);
 int mpgpu_set_stream(mpgpu_handle* h, void* cuda_stream);
 void* mpgpu_get_stream(mpgpu_handle* h);
 int mpgpu_synchronize(mpgpu_handle* h);
+/* device-to-device copy on the handle's stream (raw record buffers) */
+int mpgpu_copy_device(mpgpu_handle* h, void* dst, const void* src, size_t bytes);
 
 /* device limb count used for a precision (0 if prec is outside [2, MPGPU_MAX_PREC]) */
 int mpgpu_nlimbs_for(int32_t prec);
@@ -146,6 +149,28 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
  * the LU tolerance). */
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b,
                    mpgpu_mat* x, int exact, int64_t* zero_pivot);
+
+/* ---- multi-GPU building blocks -------------------------------------------
+ * A strided window of a device matrix (no copy; not owned). */
+int mpgpu_matrix_view(const mpgpu_mat* parent, int64_t r0, int64_t c0, int64_t rows, int64_t cols,
+                      mpgpu_mat* out);
+/* Recursion facts of fast_mul: out5 = {depth d, leaves 7^d, leaf m, leaf l, leaf n}. */
+int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out5);
+/* Sharded Strassen / Winograd (fastmm.hpp:99-229 split at the bottom of the
+ * recursion).  Nodes of level t are numbered breadth-first (child c of node p is
+ * 7p + c; level d holds the 7^d leaves).  mpgpu_fast_leaves computes the products
+ * of the level-(d - up_levels) nodes [node_lo, node_hi) -- their leaves' GEMMs plus
+ * up_levels post-addition levels -- into the device buffer node_products (node-
+ * major, node m x n records of mpgpu_record_words(nlimbs) words), running only the
+ * pre-additions of their ancestors.  mpgpu_fast_combine then runs the remaining
+ * post-addition levels from the products of ALL level-(d - up_levels) nodes (e.g.
+ * after an NCCL all-gather) into C.  The pair is bit-identical to
+ * mpgpu_gemm(STRASSEN / WINOGRAD). */
+int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                      int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products,
+                      mpgpu_stats* stats);
+int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
+                       const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats);
 
 /* ---- host-side model / plan / inputs ------------------------------------ */
 /* count_fast (opmodel.hpp:30-44); SIMPLE / BLOCK give count_simple */

@@ -14,7 +14,7 @@ LIB_PATH = Path(os.environ.get("MPGPU_LIB", Path(__file__).resolve().parent / "l
 if not LIB_PATH.exists():
     raise ImportError(
         f"libmpgpu.so not found at {LIB_PATH}: build it with "
-        "`python -m paper_1410_1599_b200.build` (or __graft_entry__.build())")
+        "`python paper_1410_1599_b200/build.py` (or __graft_entry__.build())")
 
 lib = C.CDLL(str(LIB_PATH))
 
@@ -47,6 +47,7 @@ _SIGS = {
     "mpgpu_set_stream": (C.c_int, [vp, vp]),
     "mpgpu_get_stream": (vp, [vp]),
     "mpgpu_synchronize": (C.c_int, [vp]),
+    "mpgpu_copy_device": (C.c_int, [vp, vp, vp, C.c_size_t]),
     "mpgpu_nlimbs_for": (C.c_int, [C.c_int32]),
     "mpgpu_record_words": (C.c_int, [C.c_int32]),
     "mpgpu_alloc_matrix": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int32, MatP]),
@@ -61,6 +62,11 @@ _SIGS = {
     "mpgpu_vec_op": (C.c_int, [vp, C.c_int, MatP, MatP, MatP]),
     "mpgpu_lu_blocked": (C.c_int, [vp, MatP, C.c_int64, C.c_int, C.c_int64, C.c_int, vp, i64p, StatsP]),
     "mpgpu_lu_solve": (C.c_int, [vp, MatP, vp, MatP, MatP, C.c_int, i64p]),
+    "mpgpu_matrix_view": (C.c_int, [MatP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, MatP]),
+    "mpgpu_fast_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p]),
+    "mpgpu_fast_leaves": (C.c_int, [vp, C.c_int, C.c_int64, MatP, MatP, C.c_int, C.c_int64, C.c_int64, vp,
+                                    StatsP]),
+    "mpgpu_fast_combine": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, MatP, StatsP]),
     "mpgpu_count_fast": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, u64p]),
     "mpgpu_recursion_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int,
                                        C.POINTER(C.c_int)]),

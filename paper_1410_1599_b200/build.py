@@ -1,7 +1,7 @@
 """Build libmpgpu.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels
 with the repository snapshot to the GPU box).
 
-    python -m paper_1410_1599_b200.build [--force]
+    python paper_1410_1599_b200/build.py [--force]
 """
 from __future__ import annotations
 

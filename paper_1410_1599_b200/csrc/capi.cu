@@ -308,6 +308,197 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
   return MPGPU_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Leaf-sharded fast multiply (multi-GPU building blocks).  Leaves are numbered in
+// the BFS order of run_gemm (child c of node p is 7p + c).  run_fast_leaves
+// computes the products of leaves [lo, hi) into `out` (leaf-major, m_d x n_d
+// records each), running at every level only the pre-additions of the ancestors of
+// those leaves; run_fast_combine runs all post-addition levels from the full set of
+// leaf products.  Together they reproduce run_gemm bit for bit.
+// ---------------------------------------------------------------------------
+template <int L>
+int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A, int64_t lda, const uint32_t* B,
+                    int64_t ldb, int64_t m, int64_t l, int64_t n, int64_t ulo, int64_t uhi, int up_levels,
+                    uint32_t* out, int sh, mpgpu_stats* stats) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  const bool timing = stats != nullptr;
+  Timer total(timing, st);
+  const std::vector<Level> lv = plan_levels(m, l, n, n_min);
+  const int d = (int)lv.size() - 1;
+  if (d == 0) return fail(h, MPGPU_ERR_DOMAIN, "fast_leaves: the product is a base case (depth 0)");
+  if (up_levels < 0 || up_levels > d) return fail(h, MPGPU_ERR_DIMENSION, "fast_leaves: bad output level");
+  const int ol = d - up_levels;  // level of the output nodes
+  int64_t units = 1, span = 1;  // nodes at level ol; leaves per unit
+  for (int i = 0; i < ol; ++i) units *= 7;
+  for (int i = 0; i < up_levels; ++i) span *= 7;
+  if (ulo < 0 || uhi > units || ulo >= uhi) return fail(h, MPGPU_ERR_DIMENSION, "fast_leaves: bad node range");
+  const int64_t lo = ulo * span, hi = uhi * span;
+  int launches = 0;
+  // node range needed at each level: level lev covers [s[lev], e[lev])
+  std::vector<int64_t> s(d + 1), e(d + 1);
+  s[d] = lo;
+  e[d] = hi;
+  for (int lev = d - 1; lev >= 0; --lev) {
+    s[lev] = s[lev + 1] / 7;
+    e[lev] = (e[lev + 1] + 6) / 7;
+  }
+  DevBuf a0, b0;
+  const uint32_t* pa = A;
+  const uint32_t* pb = B;
+  if (lda != l) {
+    CUDA_TRY(h, a0.alloc(h, sizeof(uint32_t) * S * m * l));
+    mpg::launch_copy2d<L>(A, lda, a0.u32(), l, (int)m, (int)l, st);
+    pa = a0.u32();
+  }
+  if (ldb != n) {
+    CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * l * n));
+    mpg::launch_copy2d<L>(B, ldb, b0.u32(), n, (int)l, (int)n, st);
+    pb = b0.u32();
+  }
+  // buffers: level lev holds nodes [bs[lev], bs[lev] + bn[lev])
+  std::vector<DevBuf> opA(d + 1), opB(d + 1);
+  std::vector<int64_t> bs(d + 1), bn(d + 1);
+  bs[0] = 0;
+  bn[0] = 1;
+  Timer tpre(timing, st);
+  for (int lev = 0; lev < d; ++lev) {
+    const Level& P = lv[lev];
+    const Level& Q = lv[lev + 1];
+    const int64_t p0 = s[lev], np = e[lev] - s[lev];
+    const uint32_t* srcA = lev == 0 ? pa : opA[lev].u32() + (p0 - bs[lev]) * P.m * P.l * S;
+    const uint32_t* srcB = lev == 0 ? pb : opB[lev].u32() + (p0 - bs[lev]) * P.l * P.n * S;
+    bs[lev + 1] = 7 * p0;
+    bn[lev + 1] = 7 * np;
+    CUDA_TRY(h, opA[lev + 1].alloc(h, sizeof(uint32_t) * S * bn[lev + 1] * Q.m * Q.l));
+    CUDA_TRY(h, opB[lev + 1].alloc(h, sizeof(uint32_t) * S * bn[lev + 1] * Q.l * Q.n));
+    mpg::launch_preadd<L>(algo, 0, srcA, np, (int)P.m, (int)P.l, opA[lev + 1].u32(), sh, h->d_err, st);
+    mpg::launch_preadd<L>(algo, 1, srcB, np, (int)P.l, (int)P.n, opB[lev + 1].u32(), sh, h->d_err, st);
+    launches += 2;
+    if (lev > 0) {
+      opA[lev].release();
+      opB[lev].release();
+    }
+  }
+  if (stats) stats->preadd_ms = tpre.stop();
+  const Level& D = lv[d];
+  {
+    Timer tl(timing, st);
+    mpg::GemmArgs g{};
+    g.A = opA[d].u32() + (lo - bs[d]) * D.m * D.l * S;
+    g.B = opB[d].u32() + (lo - bs[d]) * D.l * D.n * S;
+    DevBuf leafbuf;
+    if (up_levels == 0) {
+      g.C = out;
+    } else {
+      CUDA_TRY(h, leafbuf.alloc(h, sizeof(uint32_t) * S * (hi - lo) * D.m * D.n));
+      g.C = leafbuf.u32();
+    }
+    g.strideA = D.m * D.l;
+    g.strideB = D.l * D.n;
+    g.strideC = D.m * D.n;
+    g.lda = D.l;
+    g.ldb = D.n;
+    g.ldc = D.n;
+    g.m = (int)D.m;
+    g.l = (int)D.l;
+    g.n = (int)D.n;
+    g.kb = (int)D.l;
+    g.batch = (int)(hi - lo);
+    g.sh = sh;
+    g.err = h->d_err;
+    mpg::launch_gemm<L>(g, st);
+    ++launches;
+    if (stats) {
+      stats->leaf_ms = tl.stop();
+      stats->leaf_madds = (uint64_t)(hi - lo) * D.m * D.l * D.n;
+    }
+    opA[d].release();
+    opB[d].release();
+    // local post-additions up to level ol for the owned (whole) subtrees
+    Timer tpost(timing, st);
+    DevBuf cur_owner;
+    const uint32_t* cur = leafbuf.u32();
+    int64_t nodes = hi - lo;
+    for (int k = 0; k < up_levels; ++k) {
+      nodes /= 7;
+      const Level& P = lv[d - 1 - k];
+      uint32_t* dst;
+      DevBuf next;
+      if (k == up_levels - 1) {
+        dst = out;
+      } else {
+        CUDA_TRY(h, next.alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
+        dst = next.u32();
+      }
+      mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st);
+      ++launches;
+      if (k == 0) leafbuf.release();
+      cur_owner.release();
+      if (k != up_levels - 1) {
+        std::swap(cur_owner.p, next.p);
+        cur_owner.h = h;
+        cur = cur_owner.u32();
+      }
+    }
+    if (stats) stats->postadd_ms = tpost.stop();
+  }
+  if (stats) {
+    stats->device_ms = total.stop();
+    stats->launches = launches;
+    stats->depth = d;
+  }
+  return MPGPU_OK;
+}
+
+template <int L>
+int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* leafprods, int in_up, int64_t m,
+                     int64_t l, int64_t n, uint32_t* C, int64_t ldc, int sh, mpgpu_stats* stats) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  Timer tpost(stats != nullptr, st);
+  const std::vector<Level> lv = plan_levels(m, l, n, n_min);
+  const int d = (int)lv.size() - 1;
+  if (d == 0) return fail(h, MPGPU_ERR_DOMAIN, "fast_combine: the product is a base case (depth 0)");
+  if (in_up < 0 || in_up >= d) return fail(h, MPGPU_ERR_DIMENSION, "fast_combine: bad input level");
+  const int il = d - in_up;  // level of the given node products
+  int64_t nodes = 1;
+  for (int i = 0; i < il; ++i) nodes *= 7;
+  std::vector<DevBuf> prod(d + 1);
+  const uint32_t* cur = leafprods;
+  DevBuf top;
+  int launches = 0;
+  for (int lev = il - 1; lev >= 0; --lev) {
+    nodes /= 7;
+    const Level& P = lv[lev];
+    uint32_t* dst;
+    if (lev == 0 && ldc == n) {
+      dst = C;
+    } else if (lev == 0) {
+      CUDA_TRY(h, top.alloc(h, sizeof(uint32_t) * S * m * n));
+      dst = top.u32();
+    } else {
+      CUDA_TRY(h, prod[lev].alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
+      dst = prod[lev].u32();
+    }
+    mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st);
+    ++launches;
+    if (lev + 1 < il) prod[lev + 1].release();
+    cur = dst;
+  }
+  if (top.p) {
+    mpg::launch_copy2d<L>(top.u32(), n, C, ldc, (int)m, (int)n, st);
+    ++launches;
+  }
+  if (stats) {
+    stats->postadd_ms = tpost.stop();
+    stats->device_ms = stats->postadd_ms;
+    stats->launches = launches;
+    stats->depth = d;
+  }
+  return MPGPU_OK;
+}
+
 int validate_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B,
                   const mpgpu_mat* C) {
   if (!A || !B || !C) return fail(h, MPGPU_ERR_DIMENSION, "null matrix");
@@ -435,6 +626,14 @@ void* mpgpu_get_stream(mpgpu_handle* h) { return h ? (void*)h->stream : nullptr;
 int mpgpu_synchronize(mpgpu_handle* h) {
   if (!h) return MPGPU_ERR_DOMAIN;
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return MPGPU_OK;
+}
+
+int mpgpu_copy_device(mpgpu_handle* h, void* dst, const void* src, size_t bytes) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, h->stream));
   return MPGPU_OK;
 }
 
@@ -819,6 +1018,72 @@ int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, cons
     return fail(h, MPGPU_ERR_SINGULAR, "zero pivot at index %lld", (long long)zpv);
   }
   return rc;
+}
+
+int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out5) {
+  if (n_min < 1 || m < 1 || l < 1 || n < 1) return MPGPU_ERR_DIMENSION;
+  const std::vector<Level> lv = plan_levels(m, l, n, n_min);
+  const int d = (int)lv.size() - 1;
+  int64_t leaves = 1;
+  for (int i = 0; i < d; ++i) leaves *= 7;
+  out5[0] = d;
+  out5[1] = leaves;
+  out5[2] = lv[d].m;
+  out5[3] = lv[d].l;
+  out5[4] = lv[d].n;
+  return MPGPU_OK;
+}
+
+int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                      int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products, mpgpu_stats* stats) {
+  if (!h || !A || !B || !node_products) return MPGPU_ERR_DOMAIN;
+  if (A->cols != B->rows) return fail(h, MPGPU_ERR_DIMENSION, "inner dimension mismatch");
+  if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
+    return fail(h, MPGPU_ERR_DOMAIN, "fast_mul: algorithm must be strassen or winograd");
+  if (A->prec != B->prec || A->nlimbs != B->nlimbs) return fail(h, MPGPU_ERR_DOMAIN, "one precision required");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  if (stats) std::memset(stats, 0, sizeof *stats);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * A->nlimbs - A->prec;
+  int rc = dispatch_L(A->nlimbs, [&](auto Lc) {
+    return run_fast_leaves<decltype(Lc)::value>(h, algo, n_min, A->rec, A->ld, B->rec, B->ld, A->rows, A->cols,
+                                                B->cols, node_lo, node_hi, up_levels, node_products, sh, stats);
+  });
+  if (rc) return rc;
+  return check_err(h);
+}
+
+int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
+                       const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats) {
+  if (!h || !C || !node_products) return MPGPU_ERR_DOMAIN;
+  if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
+    return fail(h, MPGPU_ERR_DOMAIN, "fast_mul: algorithm must be strassen or winograd");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  if (stats) std::memset(stats, 0, sizeof *stats);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * C->nlimbs - C->prec;
+  int rc = dispatch_L(C->nlimbs, [&](auto Lc) {
+    return run_fast_combine<decltype(Lc)::value>(h, algo, n_min, node_products, up_levels, C->rows, l, C->cols,
+                                                 C->rec, C->ld, sh, stats);
+  });
+  if (rc) return rc;
+  return check_err(h);
+}
+
+int mpgpu_matrix_view(const mpgpu_mat* parent, int64_t r0, int64_t c0, int64_t rows, int64_t cols, mpgpu_mat* out) {
+  if (!parent || !out) return MPGPU_ERR_DOMAIN;
+  if (rows < 1 || cols < 1 || r0 < 0 || c0 < 0 || r0 + rows > parent->rows || c0 + cols > parent->cols)
+    return MPGPU_ERR_DIMENSION;
+  *out = *parent;
+  out->rows = rows;
+  out->cols = cols;
+  out->rec = parent->rec + (r0 * parent->ld + c0) * rec_stride(parent->nlimbs);
+  out->owned = 0;
+  return MPGPU_OK;
 }
 
 int mpgpu_count_fast(int algo, int64_t m, int64_t l, int64_t n, int64_t n_min, uint64_t* out2) {

@@ -20,7 +20,7 @@
 #include "mp_arith.cuh"
 
 #ifndef MPG_MINB_8
-#define MPG_MINB_8 3
+#define MPG_MINB_8 4
 #endif
 #define MPG_MINB_1 4
 #define MPG_MINB_2 4
@@ -44,44 +44,46 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+#ifndef MPG_U_8
+#define MPG_U_8 1
+#endif
+
+// per-L tiling: TM x (TN*U) outputs per CTA of TM*TN threads, each thread owning U
+// outputs of one row (columns tx, tx+TN, ...) -- U independent accumulation chains
+// per thread share the a-record
 template <int L>
 struct GemmCfg;
 template <>
 struct GemmCfg<1> {
-  static constexpr int MINB = MPG_MINB_1;
-  static constexpr int TM = 16, TN = 16, TK = 16;
+  static constexpr int MINB = MPG_MINB_1, TM = 16, TN = 16, TK = 16, U = 1;
 };
 template <>
 struct GemmCfg<2> {
-  static constexpr int MINB = MPG_MINB_2;
-  static constexpr int TM = 16, TN = 16, TK = 16;
+  static constexpr int MINB = MPG_MINB_2, TM = 16, TN = 16, TK = 16, U = 1;
 };
 template <>
 struct GemmCfg<4> {
-  static constexpr int MINB = MPG_MINB_4;
-  static constexpr int TM = 16, TN = 16, TK = 16;
+  static constexpr int MINB = MPG_MINB_4, TM = 16, TN = 16, TK = 16, U = 1;
 };
 template <>
 struct GemmCfg<8> {
-  static constexpr int MINB = MPG_MINB_8;
-  static constexpr int TM = 16, TN = 16, TK = 16;
+  static constexpr int MINB = MPG_MINB_8, TM = 16, TN = 16, TK = 16, U = MPG_U_8;
 };
 template <>
 struct GemmCfg<16> {
-  static constexpr int MINB = MPG_MINB_16;
-  static constexpr int TM = 8, TN = 16, TK = 8;
+  static constexpr int MINB = MPG_MINB_16, TM = 8, TN = 16, TK = 8, U = 1;
 };
 template <>
 struct GemmCfg<32> {
-  static constexpr int MINB = MPG_MINB_32;
-  static constexpr int TM = 8, TN = 16, TK = 4;
+  static constexpr int MINB = MPG_MINB_32, TM = 8, TN = 16, TK = 4, U = 1;
 };
 
-template <int L, int TM, int TN, int TK>
+template <int L, int TM, int TN, int TK, int U>
 __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(const GemmArgs g) {
   constexpr int S = rec_stride(L);
   constexpr int NT = TM * TN;
-  constexpr int A_WORDS = TM * TK * S, B_WORDS = TK * TN * S;
+  constexpr int TNB = TN * U;  // CTA tile width
+  constexpr int A_WORDS = TM * TK * S, B_WORDS = TK * TNB * S;
   constexpr bool A_STREAM = (L >= 16);  // large L: a-limbs read from smem inside the product
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* sA = smem;
@@ -89,13 +91,13 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 
   const int tid = threadIdx.x, tx = tid % TN, ty = tid / TN;
   const int z = blockIdx.z;
-  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TNB;
   const uint32_t* A = g.A + (int64_t)z * g.strideA * S;
   const uint32_t* B = g.B + (int64_t)z * g.strideB * S;
   uint32_t* C = g.C + (int64_t)z * g.strideC * S;
   const int KT = (g.l + TK - 1) / TK;
-  const int i = i0 + ty, j = j0 + tx;
-  const bool active = (i < g.m) && (j < g.n);
+  const int i = i0 + ty;
+  const bool active = (i < g.m) && (j0 + tx < g.n);
 
   auto stage = [&](int kt, int buf) {
     const int k0 = kt * TK;
@@ -110,9 +112,9 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
       cp_async16(sA + buf * A_WORDS + e * S + 4 * w, src, ok ? 16 : 0);
     }
 #pragma unroll 1
-    for (int c = tid; c < TK * TN * CH; c += NT) {
+    for (int c = tid; c < TK * TNB * CH; c += NT) {
       const int e = c / CH, w = c - e * CH;
-      const int kk = e / TN, cc = e - kk * TN;
+      const int kk = e / TNB, cc = e - kk * TNB;
       const int gk = k0 + kk, gj = j0 + cc;
       const bool ok = gk < g.l && gj < g.n;
       const uint32_t* src = B + ((int64_t)(ok ? gk : 0) * g.ldb + (ok ? gj : 0)) * S + 4 * w;
@@ -124,9 +126,12 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
   // included), so "C = P" for the first Block k-tile and "acc = first product" are
   // the same rounded add as every later step -- no data-dependent copies in the
   // hot loop (matrix.hpp:147-155, :203-212).
-  MP<L> acc, pacc;
-  mp_zero(acc, 1u);
-  mp_zero(pacc, 1u);
+  MP<L> acc[U], pacc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    mp_zero(acc[u], 1u);
+    mp_zero(pacc[u], 1u);
+  }
   int next_b = g.kb;  // k at which the next Block k-tile starts
 
   stage(0, 0);
@@ -144,51 +149,61 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
         if (k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
-          mp_add<L>(acc, pacc, 0u, g.sh, acc);
-          mp_zero(pacc, 1u);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            mp_add<L>(acc[u], pacc[u], 0u, g.sh, acc[u]);
+            mp_zero(pacc[u], 1u);
+          }
           next_b += g.kb;
         }
-        MP<L> b, t;
-        MPG_LOAD<L>(b_cols + kk * TN * S, b);
         const uint32_t* ar = a_rows + kk * S;
-        if constexpr (A_STREAM) {
-          mp_mul_g<L>([&](int q) { return ar[q]; }, (int32_t)ar[L], ar[L + 1], b, g.sh, t);
-        } else {
-          MP<L> a;
-          MPG_LOAD<L>(ar, a);
-          mp_mul<L>(a, b, g.sh, t);
+        MP<L> a;
+        if constexpr (!A_STREAM) MPG_LOAD<L>(ar, a);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          MP<L> b, t;
+          MPG_LOAD<L>(b_cols + (kk * TNB + u * TN) * S, b);
+          if constexpr (A_STREAM) {
+            mp_mul_g<L>([&](int q) { return ar[q]; }, (int32_t)ar[L], ar[L + 1], b, g.sh, t);
+          } else {
+            mp_mul<L>(a, b, g.sh, t);
+          }
+          mp_add<L>(pacc[u], t, 0u, g.sh, pacc[u]);
         }
-        mp_add<L>(pacc, t, 0u, g.sh, pacc);
       }
     }
     __syncthreads();
   }
   if (!active) return;
-  MP<L> res;
-  mp_add<L>(acc, pacc, 0u, g.sh, res);
-  uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
-  if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
-    MP<L> old, r;
-    load_rec<L>(cr, old);
-    mp_add<L>(old, res, 1u, g.sh, r);
-    res = r;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = j0 + tx + u * TN;
+    if (j >= g.n) break;
+    MP<L> res;
+    mp_add<L>(acc[u], pacc[u], 0u, g.sh, res);
+    uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
+    if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
+      MP<L> old;
+      load_rec<L>(cr, old);
+      mp_add<L>(old, res, 1u, g.sh, res);
+    }
+    if (exp_out_of_range(res.e)) atomicOr(g.err, ERR_EXP_RANGE);
+    store_rec<L>(cr, res);
   }
-  if (exp_out_of_range(res.e)) atomicOr(g.err, ERR_EXP_RANGE);
-  store_rec<L>(cr, res);
 }
 
 template <int L>
 void launch_gemm(const GemmArgs& g, cudaStream_t st) {
-  constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK;
+  constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
   constexpr int S = rec_stride(L);
-  const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * S);
-  auto kern = gemm_leaf_kernel<L, TM, TN, TK>;
+  const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
+  auto kern = gemm_leaf_kernel<L, TM, TN, TK, U>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  dim3 grid((g.n + TN - 1) / TN, (g.m + TM - 1) / TM, g.batch);
+  dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, g.batch);
   kern<<<grid, TM * TN, smem, st>>>(g);
 }
 

@@ -1,15 +1,77 @@
-"""Multi-GPU execution of one MP GEMM step (one process per GPU).
+"""Multi-GPU execution of one MP GEMM (one process per GPU, torch.distributed
+plumbing, NCCL for the one exchange step).  DESIGN.md section 6.
 
-Round-1 state: replicas -- every rank runs the full product on its own copy of the
-inputs (weak scaling: per-GPU work fixed as N grows).  The leaf-sharded Winograd
-(7^d leaves split over ranks, post-additions after an exchange of level-(d-1)
-products) is described in DESIGN.md "Multi-GPU" and lands in a later round.
+Strassen / Winograd (fastmm.hpp:99-229): the recursion tree is split at the bottom.
+Every rank runs the pre-additions of the ancestors of its own units only, the leaf
+GEMMs of its units, and (when units are whole sibling groups) the first post-addition
+level locally; one all-gather of the unit products then gives every rank all of
+them, and the remaining post-addition levels (a few percent of the work) run on
+each rank.  Elementwise post-additions commute with the split, so the result is
+bit-identical to the single-GPU product (and to the reference).  There is no
+all-reduce: MP rounded sums are not an NCCL reduction and are order-sensitive.
+
+Simple / Block (matrix.hpp:178-233): C is split by row blocks (row i of C depends on
+row i of A and all of B; Block's k-tiles are row-independent), then all-gathered.
+
+The partition arithmetic is pure Python (tested with world_size 2 on gloo).
 """
 from __future__ import annotations
 
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import List, Tuple
+
+from . import _lib as _L
+
+
+@dataclass(frozen=True)
+class Shard:
+    lo: int      # first unit owned by this rank
+    hi: int      # one past the last unit owned
+    per: int     # units per rank slot (ranks are padded to `per` for all_gather)
+
+
+def even_ranges(units: int, world: int) -> List[Shard]:
+    """Contiguous, padded ranges: rank r owns [r*per, min((r+1)*per, units)), so the
+    all-gathered buffer holds unit u at slot u (padding only after the last unit)."""
+    per = max(1, math.ceil(units / world))
+    return [Shard(min(r * per, units), min((r + 1) * per, units), per) for r in range(world)]
+
+
+def choose_split(depth: int, world: int) -> int:
+    """up_levels in {0, 1}: 0 splits individual leaves (7^d units, leaf products
+    exchanged), 1 splits sibling groups (7^(d-1) units, 4/7 of the bytes exchanged
+    and the first post-addition level done locally).  Take groups unless that makes
+    the busiest rank's leaf work more than 5 % above the leaf split's."""
+    if depth < 2:
+        return 0
+    leaves = 7 ** depth
+    busiest_leaf = math.ceil(leaves / world)
+    busiest_group = 7 * math.ceil(leaves // 7 / world)
+    return 1 if busiest_group <= 1.05 * busiest_leaf else 0
+
+
+def fast_plan(m: int, l: int, n: int, n_min: int) -> Tuple[int, int, int, int, int]:
+    """(depth, leaves, leaf_m, leaf_l, leaf_n) -- mpgpu_fast_plan."""
+    out = (C.c_int64 * 5)()
+    rc = _L.lib.mpgpu_fast_plan(m, l, n, n_min, out)
+    if rc:
+        raise ValueError("fast_plan: bad arguments")
+    return tuple(int(v) for v in out)
+
+
+def node_dims(m: int, l: int, n: int, n_min: int, level: int) -> Tuple[int, int]:
+    """(rows, cols) of a level-`level` node's product."""
+    for _ in range(level):
+        m, n = (m + m % 2) // 2, (n + n % 2) // 2
+    return m, n
+
 
 class _Replica:
+    """Every rank multiplies its own copy (weak scaling, no exchange)."""
     replicated = True
+    mode = "replicas"
 
     def __init__(self, algo, param, da, db, dc):
         self.algo, self.param, self.da, self.db, self.dc = algo, param, da, db, dc
@@ -19,5 +81,110 @@ class _Replica:
         return gemm_into(self.algo, self.param, self.da, self.db, self.dc)
 
 
-def make_runner(algo, param, da, db, dc, rank: int, world: int):
-    return _Replica(algo, param, da, db, dc)
+class _FastSharded:
+    replicated = False
+    mode = "leaf-shard"
+
+    def __init__(self, algo, n_min, da, db, dc, rank, world, group=None):
+        import torch
+        from .mpmm import record_words
+        self.algo, self.n_min, self.da, self.db, self.dc = int(algo), n_min, da, db, dc
+        self.group = group
+        m, l, n = da.rows(), da.cols(), db.cols()
+        self.l = l
+        depth, leaves, *_ = fast_plan(m, l, n, n_min)
+        if depth == 0:
+            raise ValueError("leaf sharding needs a recursion (depth >= 1)")
+        self.up = choose_split(depth, world)
+        units = 7 ** (depth - self.up)
+        self.shard = even_ranges(units, world)[rank]
+        um, un = node_dims(m, l, n, n_min, depth - self.up)
+        words = um * un * record_words(dc.m.nlimbs)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.local = torch.zeros(self.shard.per * words, dtype=torch.int32, device=dev)
+        self.all = torch.zeros(world * self.shard.per * words, dtype=torch.int32, device=dev)
+        self.mode = f"leaf-shard(up={self.up}, units={units}, per_rank={self.shard.per})"
+
+    def __call__(self):
+        import torch.distributed as dist
+        from .mpmm import Stats, _raise
+        st = _L.MpgpuStats()
+        h = self.dc._h
+        if self.shard.hi > self.shard.lo:
+            _raise(h, _L.lib.mpgpu_fast_leaves(h, self.algo, self.n_min, C.byref(self.da.m), C.byref(self.db.m),
+                                               self.up, self.shard.lo, self.shard.hi,
+                                               C.c_void_p(self.local.data_ptr()), C.byref(st)))
+        dist.all_gather_into_tensor(self.all, self.local, group=self.group)
+        st2 = _L.MpgpuStats()
+        _raise(h, _L.lib.mpgpu_fast_combine(h, self.algo, self.n_min, self.l, self.up,
+                                            C.c_void_p(self.all.data_ptr()), C.byref(self.dc.m), C.byref(st2)))
+        s = Stats.of(st)
+        s.postadd_ms += st2.postadd_ms
+        s.launches += st2.launches
+        s.mul, s.addsub = _count(self.algo, self.da, self.db, self.n_min)
+        return s
+
+
+class _RowSharded:
+    replicated = False
+    mode = "row-shard"
+
+    def __init__(self, algo, param, da, db, dc, rank, world, group=None):
+        import torch
+        from .mpmm import record_words
+        self.algo, self.param, self.da, self.db, self.dc, self.group = int(algo), param, da, db, dc, group
+        m, n = da.rows(), db.cols()
+        self.shard = even_ranges(m, world)[rank]
+        self.words_per_row = n * record_words(dc.m.nlimbs)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.all = torch.zeros(world * self.shard.per * self.words_per_row, dtype=torch.int32, device=dev)
+        self.local = self.all.narrow(0, rank * self.shard.per * self.words_per_row,
+                                     self.shard.per * self.words_per_row)
+        self.mode = f"row-shard(rows_per_rank={self.shard.per})"
+
+    def __call__(self):
+        import torch.distributed as dist
+        from .mpmm import Stats, _raise
+        st = _L.MpgpuStats()
+        h = self.dc._h
+        rows = self.shard.hi - self.shard.lo
+        if rows > 0:
+            av, cv = _L.MpgpuMat(), _L.MpgpuMat()
+            _L.lib.mpgpu_matrix_view(C.byref(self.da.m), self.shard.lo, 0, rows, self.da.cols(), C.byref(av))
+            # C rows land directly in this rank's slot of the gather buffer
+            cv.rows, cv.cols, cv.prec, cv.nlimbs = rows, self.db.cols(), self.dc.m.prec, self.dc.m.nlimbs
+            cv.rec, cv.ld, cv.owned = self.local.data_ptr(), self.db.cols(), 0
+            _raise(h, _L.lib.mpgpu_gemm(h, self.algo, self.param, C.byref(av), C.byref(self.db), C.byref(cv),
+                                        C.byref(st)))
+        dist.all_gather_into_tensor(self.all, self.local.clone(), group=self.group)
+        # assemble C (rows beyond m are padding)
+        nbytes = self.dc.rows() * self.words_per_row * 4
+        _cuda_copy(h, self.dc.data_ptr, self.all.data_ptr(), nbytes)
+        s = Stats.of(st)
+        s.mul, s.addsub = _count(self.algo, self.da, self.db, self.param)
+        return s
+
+
+def _count(algo, da, db, param):
+    out = (C.c_uint64 * 2)()
+    _L.lib.mpgpu_count_fast(int(algo), da.rows(), da.cols(), db.cols(), max(1, param), out)
+    return int(out[0]), int(out[1])
+
+
+def _cuda_copy(h, dst: int, src: int, nbytes: int):
+    from .mpmm import _raise
+    _raise(h, _L.lib.mpgpu_copy_device(h, C.c_void_p(dst), C.c_void_p(src), C.c_size_t(nbytes)))
+
+
+def make_runner(algo, param, da, db, dc, rank: int, world: int, mode: str = "auto", group=None):
+    """mode: 'auto' (fast algorithms: leaf shards; simple/block: row shards),
+    'replicas' (independent copies, weak scaling)."""
+    from .mpmm import Algorithm
+    if world <= 1 or mode == "replicas":
+        return _Replica(algo, param, da, db, dc)
+    if Algorithm(algo) in (Algorithm.strassen, Algorithm.winograd):
+        depth, *_ = fast_plan(da.rows(), da.cols(), db.cols(), param)
+        if depth >= 1:
+            return _FastSharded(algo, param, da, db, dc, rank, world, group)
+        return _Replica(algo, param, da, db, dc)
+    return _RowSharded(algo, param, da, db, dc, rank, world, group)

@@ -154,7 +154,7 @@ class _RowSharded:
             # C rows land directly in this rank's slot of the gather buffer
             cv.rows, cv.cols, cv.prec, cv.nlimbs = rows, self.db.cols(), self.dc.m.prec, self.dc.m.nlimbs
             cv.rec, cv.ld, cv.owned = self.local.data_ptr(), self.db.cols(), 0
-            _raise(h, _L.lib.mpgpu_gemm(h, self.algo, self.param, C.byref(av), C.byref(self.db), C.byref(cv),
+            _raise(h, _L.lib.mpgpu_gemm(h, self.algo, self.param, C.byref(av), C.byref(self.db.m), C.byref(cv),
                                         C.byref(st)))
         dist.all_gather_into_tensor(self.all, self.local.clone(), group=self.group)
         # assemble C (rows beyond m are padding)

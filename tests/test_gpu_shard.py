@@ -60,5 +60,5 @@ def test_row_split_bit_exact(P, algo, param):
         av, cv = L.MpgpuMat(), L.MpgpuMat()
         assert L.lib.mpgpu_matrix_view(C.byref(da.m), r.lo, 0, rows, l, C.byref(av)) == 0
         assert L.lib.mpgpu_matrix_view(C.byref(dc.m), r.lo, 0, rows, n, C.byref(cv)) == 0
-        assert L.lib.mpgpu_gemm(h, int(P.Algorithm[algo]), param, C.byref(av), C.byref(db), C.byref(cv), None) == 0
+        assert L.lib.mpgpu_gemm(h, int(P.Algorithm[algo]), param, C.byref(av), C.byref(db.m), C.byref(cv), None) == 0
     assert P.identical(dc.download(), want)

@@ -576,6 +576,54 @@ int bitlen(const std::vector<uint32_t>& v) {
 
 }  // namespace
 
+// host SoA -> device records (stream-ordered, no sync); stage is scratch owned by the caller
+int upload_async(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_t* limbs, const int32_t* exp,
+                 const uint8_t* sign, int32_t Lh, DevBuf& stage) {
+  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
+  uint32_t* dl = stage.u32();
+  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
+  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
+  // most significant limbs aligned: host plane j <-> device plane j + (L - Lh)
+  if (Lh <= L) {
+    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
+                                cudaMemcpyHostToDevice, h->stream));
+  } else {
+    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, h->stream));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, h->stream));
+  dispatch_L(L, [&](auto Lc) {
+    mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, rec, h->stream);
+    return 0;
+  });
+  return MPGPU_OK;
+}
+
+int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint32_t* limbs, int32_t* exp,
+                   uint8_t* sign, int32_t Lh, DevBuf& stage) {
+  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
+  uint32_t* dl = stage.u32();
+  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
+  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
+  dispatch_L(L, [&](auto Lc) {
+    mpg::launch_rec2soa<decltype(Lc)::value>(rec, N, dl, de, ds, N, h->stream);
+    return 0;
+  });
+  if (Lh <= L) {
+    CUDA_TRY(h, cudaMemcpyAsync(limbs, dl + (size_t)(L - Lh) * N, sizeof(uint32_t) * (size_t)Lh * N,
+                                cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    std::memset(limbs, 0, sizeof(uint32_t) * (size_t)(Lh - L) * N);
+    CUDA_TRY(h, cudaMemcpyAsync(limbs + (size_t)(Lh - L) * N, dl, planes, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(exp, de, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(sign, ds, N, cudaMemcpyDeviceToHost, h->stream));
+  return MPGPU_OK;
+}
+
 // ===========================================================================
 extern "C" {
 
@@ -688,31 +736,12 @@ int mpgpu_upload(mpgpu_handle* h, mpgpu_mat* m, const uint32_t* limbs, const int
                  int32_t Lh) {
   if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
   if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "upload into a strided view");
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   std::lock_guard<std::mutex> lk(h->mu);
   cudaSetDevice(h->device);
-  const int L = m->nlimbs;
-  const int64_t N = m->rows * m->cols;
-  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   DevBuf stage;
-  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
-  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
-  uint32_t* dl = stage.u32();
-  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
-  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
-  // most significant limbs aligned: host plane j <-> device plane j + (L - Lh)
-  if (Lh <= L) {
-    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, h->stream));
-    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
-                                cudaMemcpyHostToDevice, h->stream));
-  } else {
-    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, h->stream));
-  }
-  CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, h->stream));
-  dispatch_L(L, [&](auto Lc) {
-    mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, m->rec, h->stream);
-    return 0;
-  });
+  int rc = upload_async(h, m->rec, m->nlimbs, m->rows * m->cols, limbs, exp, sign, Lh, stage);
+  if (rc) return rc;
   stage.release();
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaGetLastError());
@@ -723,30 +752,12 @@ int mpgpu_download(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t
                    int32_t Lh) {
   if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
   if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "download from a strided view");
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   std::lock_guard<std::mutex> lk(h->mu);
   cudaSetDevice(h->device);
-  const int L = m->nlimbs;
-  const int64_t N = m->rows * m->cols;
-  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   DevBuf stage;
-  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
-  CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
-  uint32_t* dl = stage.u32();
-  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
-  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
-  dispatch_L(L, [&](auto Lc) {
-    mpg::launch_rec2soa<decltype(Lc)::value>(m->rec, N, dl, de, ds, N, h->stream);
-    return 0;
-  });
-  if (Lh <= L) {
-    CUDA_TRY(h, cudaMemcpyAsync(limbs, dl + (size_t)(L - Lh) * N, sizeof(uint32_t) * (size_t)Lh * N,
-                                cudaMemcpyDeviceToHost, h->stream));
-  } else {
-    std::memset(limbs, 0, sizeof(uint32_t) * (size_t)(Lh - L) * N);
-    CUDA_TRY(h, cudaMemcpyAsync(limbs + (size_t)(Lh - L) * N, dl, planes, cudaMemcpyDeviceToHost, h->stream));
-  }
-  CUDA_TRY(h, cudaMemcpyAsync(exp, de, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(sign, ds, N, cudaMemcpyDeviceToHost, h->stream));
+  int rc = download_async(h, m->rec, m->nlimbs, m->rows * m->cols, limbs, exp, sign, Lh, stage);
+  if (rc) return rc;
   stage.release();
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaGetLastError());
@@ -781,19 +792,47 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
                     const uint32_t* al, const int32_t* ae, const uint8_t* as, const uint32_t* bl,
                     const int32_t* be, const uint8_t* bs, uint32_t* cl, int32_t* ce, uint8_t* cs, int32_t Lh,
                     mpgpu_stats* stats) {
+  // One stream-ordered sequence: pooled device buffers, H2D + layout conversion of A
+  // and B, the product, conversion + D2H of C, and a single synchronisation.
   if (!h) return MPGPU_ERR_DOMAIN;
-  mpgpu_mat A{}, B{}, C{};
-  int rc = mpgpu_alloc_matrix(h, m, l, prec, &A);
-  if (!rc) rc = mpgpu_alloc_matrix(h, l, n, prec, &B);
-  if (!rc) rc = mpgpu_alloc_matrix(h, m, n, prec, &C);
-  if (!rc) rc = mpgpu_upload(h, &A, al, ae, as, Lh);
-  if (!rc) rc = mpgpu_upload(h, &B, bl, be, bs, Lh);
-  if (!rc) rc = mpgpu_gemm(h, algo, param, &A, &B, &C, stats);
-  if (!rc) rc = mpgpu_download(h, &C, cl, ce, cs, Lh);
-  mpgpu_free_matrix(h, &A);
-  mpgpu_free_matrix(h, &B);
-  mpgpu_free_matrix(h, &C);
-  return rc;
+  const int L = nlimbs_for(prec);
+  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
+  if (m < 1 || l < 1 || n < 1) return fail(h, MPGPU_ERR_DIMENSION, "matrix dimensions must be at least 1x1");
+  if (Lh < (prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  mpgpu_mat A{m, l, prec, L, nullptr, l, 0}, B{l, n, prec, L, nullptr, n, 0}, C{m, n, prec, L, nullptr, n, 0};
+  int rc = validate_gemm(h, algo, param, &A, &B, &C);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  const size_t S4 = sizeof(uint32_t) * rec_stride(L);
+  DevBuf da, db, dc, sa, sb, sc;
+  CUDA_TRY(h, da.alloc(h, S4 * m * l));
+  CUDA_TRY(h, db.alloc(h, S4 * l * n));
+  CUDA_TRY(h, dc.alloc(h, S4 * m * n));
+  A.rec = da.u32();
+  B.rec = db.u32();
+  C.rec = dc.u32();
+  if (stats) {
+    std::memset(stats, 0, sizeof *stats);
+    uint64_t c[2];
+    count_fast_rec(algo, m, l, n, param, c);
+    stats->mul = c[0];
+    stats->addsub = c[1];
+  }
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  rc = upload_async(h, A.rec, L, m * l, al, ae, as, Lh, sa);
+  if (!rc) rc = upload_async(h, B.rec, L, l * n, bl, be, bs, Lh, sb);
+  if (rc) return rc;
+  sa.release();
+  sb.release();
+  const int sh = 32 * L - prec;
+  rc = dispatch_L(L, [&](auto Lc) {
+    return run_gemm<decltype(Lc)::value>(h, algo, param, A.rec, l, B.rec, n, C.rec, n, m, l, n, sh, stats, 0);
+  });
+  if (rc) return rc;
+  rc = download_async(h, C.rec, L, m * n, cl, ce, cs, Lh, sc);
+  if (rc) return rc;
+  return check_err(h);
 }
 
 int mpgpu_addsub(mpgpu_handle* h, int is_sub, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C) {

@@ -157,3 +157,16 @@ def test_gemm_matches_frozen_reference_fixture(P, path):
     c = _run(P, str(d["alg"]), int(d["param"]), a, b, a.ctx(), ops)
     assert P.identical(c, want)
     assert (ops.mul, ops.addsub) == tuple(int(v) for v in d["ops"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg,param", [("winograd", 8), ("block", 16), ("simple", 0)])
+def test_gemm_host_buffers_path(P, O, alg, param):
+    # mpgpu_gemm_host: the reference-facing call with host SoA buffers (bench e2e path)
+    ctx = P.PrecisionContext(200)  # host limbs 7 < device limbs 8
+    a, b = P.gen_uniform_full(40, 33, 1, ctx), P.gen_uniform_full(33, 29, 2, ctx)
+    c = P.Matrix(40, 29, ctx)
+    st = P.gemm_host(P.Algorithm[alg], param, a, b, c, ctx)
+    want, ops = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)
+    assert (st.mul, st.addsub) == ops

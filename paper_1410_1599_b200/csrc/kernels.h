@@ -83,6 +83,19 @@ template <int L>
 void launch_trsm_l_step(uint32_t* a, int64_t n, int64_t s, int64_t p_end, int64_t c0, int64_t w,
                         int sh, uint32_t* err, cudaStream_t st);
 
+// whole-panel factorisation (all pivot columns of [p, p+k), rows [p, row_end)) in one
+// cooperative launch; returns -1 if it cannot run (caller uses the per-column path).
+// cand_key / cand_idx: scratch of at least max_grid entries.
+template <int L>
+int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting,
+                         int64_t* piv, int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid,
+                         cudaStream_t st);
+
+// whole-panel trsm_unit_lower: rows [p, p+k) x cols [c0, c0+w), one launch
+template <int L>
+void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0, int64_t w, int sh,
+                         cudaStream_t st);
+
 // Ly = Pb, Ux = y on packed factors (blocklu.hpp:215-245); scratch: 2n records
 template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b,

@@ -11,6 +11,9 @@
 // pivot-free, blocklu.hpp:38-41) the pivot row is swapped in first.
 // U12: trsm_unit_lower_inplace (blocklu.hpp:60-69) is replayed as a column sweep
 // over s -- per element the same s-ascending order.
+#include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -88,54 +91,99 @@ __global__ void trsm_l_kernel(uint32_t* a, int64_t n, int64_t s, int64_t p_end, 
   }
 }
 
-// pivot search (first maximal |a_id| over rows [d, row_end)) + full-row swap
+// pivot search (first maximal |a_id| over rows [d, row_end)) + full-row swap.
+// Phase 1 reduces a 64-bit magnitude key (biased exponent : top limb) with warp
+// shuffles; rows whose key ties with the maximum are then resolved by a full MP
+// comparison (first maximal row wins), which only runs when a tie exists.
+constexpr int PIV_NT = 1024;
+__device__ __forceinline__ uint64_t mag_key(uint32_t e, uint32_t top) {
+  return e == (uint32_t)EXP_ZERO ? 0ull : (((uint64_t)(e ^ 0x80000000u)) << 32) | top;
+}
 template <int L>
-__global__ void __launch_bounds__(NT) pivot_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end,
-                                                   int64_t* piv, int64_t* zp) {
+__global__ void __launch_bounds__(PIV_NT) pivot_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end,
+                                                       int64_t* piv, int64_t* zp) {
   constexpr int S = rec_stride(L);
-  __shared__ int64_t s_idx[NT];
+  __shared__ uint64_t s_key[PIV_NT / 32];
+  __shared__ int64_t s_idx[PIV_NT / 32];
+  __shared__ uint64_t s_best_key;
   __shared__ int64_t s_best;
+  __shared__ int s_ties;
   if (*zp) return;
-  int64_t best = -1;
-  MP<L> bv;
-  mp_zero(bv);
-  for (int64_t i = d + threadIdx.x; i < row_end; i += blockDim.x) {
-    MP<L> x;
-    load_rec<L>(a + (i * n + d) * S, x);
-    if (best < 0 || mp_cmpabs<L>(x, bv) > 0) {
-      bv = x;
-      best = i;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint64_t bk = 0;
+  int64_t bi = INT64_MAX;
+  for (int64_t i = d + tid; i < row_end; i += PIV_NT) {
+    const uint32_t* r = a + (i * n + d) * S;
+    const uint64_t k = mag_key(r[L], r[L - 1]);
+    if (bi == INT64_MAX || k > bk) {
+      bk = k;
+      bi = i;
     }
   }
-  s_idx[threadIdx.x] = best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+    const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (k2 > bk || (k2 == bk && i2 < bi)) {
+      bk = k2;
+      bi = i2;
+    }
+  }
+  if (lane == 0) {
+    s_key[wid] = bk;
+    s_idx[wid] = bi;
+  }
+  if (tid == 0) s_ties = 0;
   __syncthreads();
-  // tree reduction: larger |a_id| wins, ties go to the lower row index
-  for (int half = NT / 2; half > 0; half >>= 1) {
-    if (threadIdx.x < half) {
-      const int64_t i0 = s_idx[threadIdx.x], i1 = s_idx[threadIdx.x + half];
-      if (i1 >= 0) {
-        bool take = i0 < 0;
-        if (!take) {
-          MP<L> x0, x1;
-          load_rec<L>(a + (i0 * n + d) * S, x0);
-          load_rec<L>(a + (i1 * n + d) * S, x1);
-          const int c = mp_cmpabs<L>(x1, x0);
-          take = c > 0 || (c == 0 && i1 < i0);
-        }
-        if (take) s_idx[threadIdx.x] = i1;
+  if (wid == 0) {
+    bk = s_key[lane];
+    bi = s_idx[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (k2 > bk || (k2 == bk && i2 < bi)) {
+        bk = k2;
+        bi = i2;
       }
     }
-    __syncthreads();
+    if (lane == 0) {
+      s_best_key = bk;
+      s_best = bi;
+    }
   }
-  if (threadIdx.x == 0) {
-    s_best = s_idx[0];
-    piv[d] = s_idx[0];
+  __syncthreads();
+  // ties on the compact key: count them
+  const uint64_t kstar = s_best_key;
+  int mine = 0;
+  for (int64_t i = d + tid; i < row_end; i += PIV_NT) {
+    const uint32_t* r = a + (i * n + d) * S;
+    mine += mag_key(r[L], r[L - 1]) == kstar;
+  }
+  if (mine) atomicAdd(&s_ties, mine);
+  __syncthreads();
+  if (s_ties > 1 && tid == 0) {  // rare: full comparison among the tied rows
+    int64_t r = -1;
+    MP<L> rv;
+    mp_zero(rv);
+    for (int64_t i = d; i < row_end; ++i) {
+      const uint32_t* q = a + (i * n + d) * S;
+      if (mag_key(q[L], q[L - 1]) != kstar) continue;
+      MP<L> x;
+      load_rec<L>(q, x);
+      if (r < 0 || mp_cmpabs<L>(x, rv) > 0) {
+        rv = x;
+        r = i;
+      }
+    }
+    s_best = r;
   }
   __syncthreads();
   const int64_t r = s_best;
+  if (tid == 0) piv[d] = r;
   if (r != d) {
     constexpr int CH = S / 4;
-    for (int64_t t = threadIdx.x; t < n * CH; t += blockDim.x) {
+    for (int64_t t = tid; t < n * CH; t += PIV_NT) {
       const int64_t j = t / CH, w = t % CH;
       uint4* p = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
       uint4* q = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
@@ -143,6 +191,32 @@ __global__ void __launch_bounds__(NT) pivot_kernel(uint32_t* a, int64_t n, int64
       *p = *q;
       *q = tmp;
     }
+  }
+}
+
+// trsm_unit_lower over a whole panel in one launch (blocklu.hpp:60-69): each CTA owns
+// TRSM_TC columns of U12 and sweeps s = p .. p+k-2 with a barrier per step; per
+// element the updates arrive in s-ascending order, as in the reference.
+constexpr int TRSM_TC = 4;
+template <int L>
+__global__ void __launch_bounds__(NT) trsm_l_panel_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0,
+                                                          int64_t w, int sh) {
+  constexpr int S = rec_stride(L);
+  const int64_t j0 = c0 + (int64_t)blockIdx.x * TRSM_TC;
+  const int tc = (int)(c0 + w - j0 < TRSM_TC ? c0 + w - j0 : TRSM_TC);
+  for (int64_t s = p; s + 1 < p + k; ++s) {
+    const int64_t rows = p + k - s - 1;
+    for (int64_t t = threadIdx.x; t < rows * tc; t += blockDim.x) {
+      const int64_t i = s + 1 + t / tc, j = j0 + t % tc;
+      MP<L> l, u, pr, x;
+      load_rec<L>(a + (i * n + s) * S, l);
+      load_rec<L>(a + (s * n + j) * S, u);
+      mp_mul<L>(l, u, sh, pr);
+      load_rec<L>(a + (i * n + j) * S, x);
+      mp_add<L>(x, pr, 1u, sh, x);
+      store_rec<L>(a + (i * n + j) * S, x);
+    }
+    __syncthreads();
   }
 }
 
@@ -255,6 +329,234 @@ __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-panel factorisation in ONE cooperative launch: for every pivot column d of
+// the panel [p, p+k) (rows [p, row_end)):
+//   (pivoting) per-CTA best magnitude key -> grid.sync -> every CTA reduces the same
+//   candidates (identical result) -> row swap split over CTAs -> grid.sync;
+//   multipliers (one MP division per row) and the rank-1 update of the panel
+//   columns for the CTA's own rows -> grid.sync.
+// Same per-element operation sequence as the per-column kernels (and the
+// reference), without a kernel launch per column.
+// ---------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(NT) lu_panel_coop_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k,
+                                                           int64_t row_end, int pivoting, int64_t* piv,
+                                                           int64_t* zp, int sh, uint64_t* cand_key,
+                                                           int64_t* cand_idx, uint64_t* cand_cnt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int S = rec_stride(L);
+  extern __shared__ __align__(16) uint32_t s_mult[];
+  __shared__ uint64_t s_wk[NT / 32];
+  __shared__ int64_t s_wi[NT / 32];
+  __shared__ int64_t s_piv;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t rows_all = row_end - p;
+  const int64_t chunk = (rows_all + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = p + (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(row_end, lo + chunk);
+  for (int64_t d = p; d < p + k; ++d) {
+    if (pivoting) {
+      // (1) CTA-local best (key, idx) over rows [max(d, lo), hi) and how many of
+      //     the CTA's rows share that key
+      uint64_t bk = 0;
+      int64_t bi = INT64_MAX;
+      for (int64_t i = max(d, lo) + tid; i < hi; i += NT) {
+        const uint32_t* r = a + (i * n + d) * S;
+        const uint64_t kk = mag_key(r[L], r[L - 1]);
+        if (bi == INT64_MAX || kk > bk) {
+          bk = kk;
+          bi = i;
+        }
+      }
+      auto better = [](uint64_t k1, int64_t i1, uint64_t k0, int64_t i0) {
+        return i1 != INT64_MAX && (i0 == INT64_MAX || k1 > k0 || (k1 == k0 && i1 < i0));
+      };
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(k2, i2, bk, bi)) {
+          bk = k2;
+          bi = i2;
+        }
+      }
+      if (lane == 0) {
+        s_wk[wid] = bk;
+        s_wi[wid] = bi;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        bk = lane < NT / 32 ? s_wk[lane] : 0;
+        bi = lane < NT / 32 ? s_wi[lane] : INT64_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (better(k2, i2, bk, bi)) {
+            bk = k2;
+            bi = i2;
+          }
+        }
+        if (lane == 0) {
+          s_wk[0] = bk;
+          s_wi[0] = bi;
+        }
+      }
+      __syncthreads();
+      {
+        const uint64_t kb = s_wk[0];
+        int cnt = 0;
+        for (int64_t i = max(d, lo) + tid; i < hi; i += NT) {
+          const uint32_t* r = a + (i * n + d) * S;
+          cnt += mag_key(r[L], r[L - 1]) == kb;
+        }
+        cnt = __syncthreads_count(cnt > 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0;
+        if (lane == 0 && s_wi[0] != INT64_MAX) atomicAdd(reinterpret_cast<unsigned long long*>(&cand_cnt[blockIdx.x]), (unsigned long long)cnt);
+      }
+      if (tid == 0) {
+        cand_key[blockIdx.x] = s_wk[0];
+        cand_idx[blockIdx.x] = s_wi[0];
+      }
+      grid.sync();
+      // (2) every CTA reduces the same candidate list -> the same pivot
+      {
+        uint64_t gk = 0;
+        int64_t gi = INT64_MAX;
+        for (unsigned b = tid; b < gridDim.x; b += NT) {
+          if (better(cand_key[b], cand_idx[b], gk, gi)) {
+            gk = cand_key[b];
+            gi = cand_idx[b];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, gk, o);
+          const int64_t i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+          if (better(k2, i2, gk, gi)) {
+            gk = k2;
+            gi = i2;
+          }
+        }
+        __syncthreads();
+        if (lane == 0) {
+          s_wk[wid] = gk;
+          s_wi[wid] = gi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < NT / 32; ++w)
+            if (better(s_wk[w], s_wi[w], gk, gi)) {
+              gk = s_wk[w];
+              gi = s_wi[w];
+            }
+          // rows sharing the winning compact key: a full comparison decides (rare)
+          unsigned long long ties = 0;
+          for (unsigned b = 0; b < gridDim.x; ++b)
+            if (cand_idx[b] != INT64_MAX && cand_key[b] == gk) ties += cand_cnt[b];
+          if (ties > 1) {
+            MP<L> rv, x;
+            int64_t r = -1;
+            for (int64_t i = d; i < row_end; ++i) {
+              const uint32_t* q = a + (i * n + d) * S;
+              if (mag_key(q[L], q[L - 1]) != gk) continue;
+              load_rec<L>(q, x);
+              if (r < 0 || mp_cmpabs<L>(x, rv) > 0) {
+                rv = x;
+                r = i;
+              }
+            }
+            gi = r;
+          }
+          s_piv = gi;
+          if (blockIdx.x == 0) piv[d] = gi;
+        }
+      }
+      __syncthreads();
+      const int64_t r = s_piv;
+      if (r != d) {  // (3) swap rows d, r: columns split over CTAs
+        constexpr int CH = S / 4;
+        for (int64_t t = (int64_t)blockIdx.x * NT + tid; t < n * CH; t += (int64_t)gridDim.x * NT) {
+          const int64_t j = t / CH, w = t % CH;
+          uint4* pp = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
+          uint4* qq = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
+          const uint4 tmp = *pp;
+          *pp = *qq;
+          *qq = tmp;
+        }
+      }
+      grid.sync();
+    }
+    if (pivoting && tid == 0) cand_cnt[blockIdx.x] = 0;  // read by all CTAs before the swap sync
+    // (4) zero pivot: every CTA sees the same a_dd and stops (blocklu.hpp:46-47)
+    if (a[(d * n + d) * S + L] == (uint32_t)EXP_ZERO) {
+      if (blockIdx.x == 0 && tid == 0) *zp = d + 1;
+      return;
+    }
+    // (5) multipliers and rank-1 update for this CTA's rows in (d, row_end)
+    const int64_t r0 = max(d + 1, lo);
+    const int64_t nr = hi - r0;
+    if (nr > 0) {
+      for (int64_t t = tid; t < nr; t += NT) {
+        MP<L> piv_v, x, q;
+        load_rec<L>(a + (d * n + d) * S, piv_v);
+        load_rec<L>(a + ((r0 + t) * n + d) * S, x);
+        mp_div<L>(x, piv_v, sh, q);
+        store_rec<L>(a + ((r0 + t) * n + d) * S, q);
+        store_rec<L>(s_mult + t * S, q);
+      }
+      __syncthreads();
+      const int64_t w = p + k - d - 1;
+      for (int64_t t = tid; t < nr * w; t += NT) {
+        const int64_t rr = t / w, j = d + 1 + t % w;
+        MP<L> l, u, pr, x;
+        load_rec<L>(s_mult + rr * S, l);
+        load_rec<L>(a + (d * n + j) * S, u);
+        mp_mul<L>(l, u, sh, pr);
+        load_rec<L>(a + ((r0 + rr) * n + j) * S, x);
+        mp_add<L>(x, pr, 1u, sh, x);
+        store_rec<L>(a + ((r0 + rr) * n + j) * S, x);
+      }
+    }
+    grid.sync();
+  }
+}
+
+template <int L>
+int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting,
+                         int64_t* piv, int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid,
+                         cudaStream_t st) {
+  constexpr int S = rec_stride(L);
+  uint64_t* cand_cnt = reinterpret_cast<uint64_t*>(cand_idx + max_grid);
+  static int max_blocks = 0;
+  static int dev_sms = 0;
+  const int64_t rows = row_end - p;
+  // rows per CTA bounded so the multipliers fit in shared memory
+  int64_t want = (rows + 7) / 8;
+  if (!max_blocks) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_coop_kernel<L>, NT, 16 * 1024);
+    max_blocks = per_sm * dev_sms;
+  }
+  int64_t grid = want < max_blocks ? want : max_blocks;
+  if (grid > 2 * dev_sms) grid = 2 * dev_sms;
+  if (const char* g = std::getenv("MPGPU_LU_COOP_GRID")) grid = std::min<int64_t>(grid, std::atoll(g));
+  if (grid > max_grid) grid = max_grid;
+  if (grid < 1) grid = 1;
+  // the CTA's multipliers live in shared memory: chunk rows of S words
+  const int64_t chunk = (rows + grid - 1) / grid;
+  const size_t smem = sizeof(uint32_t) * S * (size_t)chunk;
+  if (smem > 16 * 1024) return -1;  // caller falls back to per-column kernels
+  void* args[] = {&a, &n, &p, &k, &row_end, &pivoting, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)lu_panel_coop_kernel<L>, dim3((unsigned)grid), dim3(NT), args,
+                                              smem, st);
+  return e == cudaSuccess ? 0 : -1;
+}
+
 template <int L>
 void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh, uint32_t* err,
                     cudaStream_t st) {
@@ -268,7 +570,7 @@ void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t 
 template <int L>
 void launch_pivot(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t* piv_dev, int64_t* zp,
                   cudaStream_t st) {
-  pivot_kernel<L><<<1, NT, 0, st>>>(a, n, d, row_end, piv_dev, zp);
+  pivot_kernel<L><<<1, PIV_NT, 0, st>>>(a, n, d, row_end, piv_dev, zp);
 }
 
 template <int L>
@@ -277,6 +579,13 @@ void launch_trsm_l_step(uint32_t* a, int64_t n, int64_t s, int64_t p_end, int64_
   (void)err;
   const int64_t total = (p_end - s - 1) * w;
   if (total > 0) trsm_l_kernel<L><<<blocks_for(total), NT, 0, st>>>(a, n, s, p_end, c0, w, sh);
+}
+
+template <int L>
+void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0, int64_t w, int sh,
+                         cudaStream_t st) {
+  if (w <= 0 || k <= 1) return;
+  trsm_l_panel_kernel<L><<<(int)((w + TRSM_TC - 1) / TRSM_TC), NT, 0, st>>>(a, n, p, k, c0, w, sh);
 }
 
 template <int L>
@@ -291,6 +600,9 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
   template void launch_pivot<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t*, int64_t*, cudaStream_t);        \
   template void launch_trsm_l_step<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int, uint32_t*,   \
                                       cudaStream_t);                                                            \
+  template void launch_trsm_l_panel<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t); \
+  template int launch_lu_panel_coop<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int, int64_t*, int64_t*, int, \
+                                       uint64_t*, int64_t*, int, cudaStream_t);                                      \
   template void launch_lu_solve<L>(const uint32_t*, int64_t, const int64_t*, const uint32_t*, uint32_t*,        \
                                    uint32_t*, int, uint32_t*, int64_t*, int, cudaStream_t);
 MPG_LU_INST(1)

@@ -96,29 +96,59 @@ struct DevBuf {
   uint32_t* u32() const { return static_cast<uint32_t*>(p); }
 };
 
+// CUDA-event phase timers that never block: stop() records the end event and
+// queues (start, end, destination); flush_timers() (called once per API call, at
+// its final synchronisation) resolves every queued duration.  No host/GPU
+// round trip inside a call, so phases run back to back on the GPU.
+struct PendingTime {
+  cudaEvent_t a, b;
+  double* dst;
+};
+thread_local std::vector<PendingTime> g_pending;
+
+void flush_timers() {
+  for (auto& t : g_pending) {
+    cudaEventSynchronize(t.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    if (t.dst) *t.dst = ms;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  g_pending.clear();
+}
+
+// error paths: drop queued timings without writing (their destinations may be gone)
+struct TimerGuard {
+  ~TimerGuard() {
+    for (auto& t : g_pending) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    g_pending.clear();
+  }
+};
+
 struct Timer {
   bool on;
   cudaStream_t st;
-  cudaEvent_t a = nullptr, b = nullptr;
+  cudaEvent_t a = nullptr;
   Timer(bool enabled, cudaStream_t s) : on(enabled), st(s) {
     if (on) {
       cudaEventCreate(&a);
-      cudaEventCreate(&b);
       cudaEventRecord(a, st);
     }
   }
-  // returns elapsed ms (synchronises on the end event)
-  double stop() {
-    if (!on) return 0.0;
+  void stop(double* dst) {
+    if (!on || !a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
     cudaEventRecord(b, st);
-    cudaEventSynchronize(b);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, a, b);
-    return ms;
+    g_pending.push_back({a, b, dst});
+    a = nullptr;
   }
   ~Timer() {
     if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
   }
 };
 
@@ -153,6 +183,7 @@ std::vector<Level> plan_levels(int64_t m, int64_t l, int64_t n, int64_t n_min) {
 }
 
 int check_err(mpgpu_handle* h) {
+  flush_timers();
   uint32_t e = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&e, h->d_err, sizeof e, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -207,7 +238,7 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
     Timer tl(timing, st);
     leaf(A, lda, B, ldb, C, ldc, m, l, n, algo == MPGPU_SIMPLE ? l : param, 1, sub_from_c);
     if (stats) {
-      stats->leaf_ms = tl.stop();
+      tl.stop(&stats->leaf_ms);
       stats->leaf_madds = (uint64_t)m * l * n;
     }
   } else {
@@ -218,7 +249,7 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
       Timer tl(timing, st);
       leaf(A, lda, B, ldb, C, ldc, m, l, n, l, 1, sub_from_c);
       if (stats) {
-        stats->leaf_ms = tl.stop();
+        tl.stop(&stats->leaf_ms);
         stats->leaf_madds = (uint64_t)m * l * n;
       }
     } else {
@@ -259,14 +290,14 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
       }
       a0.release();
       b0.release();
-      if (stats) stats->preadd_ms = tpre.stop();
+      if (stats) tpre.stop(&stats->preadd_ms);
       const Level& D = lv[d];
       CUDA_TRY(h, prod[d].alloc(h, sizeof(uint32_t) * S * nodes * D.m * D.n));
       {
         Timer tl(timing, st);
         leaf(opA[d].u32(), D.l, opB[d].u32(), D.n, prod[d].u32(), D.n, D.m, D.l, D.n, D.l, (int)nodes, 0);
         if (stats) {
-          stats->leaf_ms = tl.stop();
+          tl.stop(&stats->leaf_ms);
           stats->leaf_madds = (uint64_t)nodes * D.m * D.l * D.n;
         }
       }
@@ -299,11 +330,11 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
         mpg::launch_copy2d<L>(top.u32(), n, C, ldc, (int)m, (int)n, st);
         ++launches;
       }
-      if (stats) stats->postadd_ms = tpost.stop();
+      if (stats) tpost.stop(&stats->postadd_ms);
     }
   }
   if (stats) {
-    stats->device_ms = total.stop();
+    total.stop(&stats->device_ms);
     stats->launches = launches;
   }
   return MPGPU_OK;
@@ -381,7 +412,7 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
       opB[lev].release();
     }
   }
-  if (stats) stats->preadd_ms = tpre.stop();
+  if (stats) tpre.stop(&stats->preadd_ms);
   const Level& D = lv[d];
   {
     Timer tl(timing, st);
@@ -411,7 +442,7 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
     mpg::launch_gemm<L>(g, st);
     ++launches;
     if (stats) {
-      stats->leaf_ms = tl.stop();
+      tl.stop(&stats->leaf_ms);
       stats->leaf_madds = (uint64_t)(hi - lo) * D.m * D.l * D.n;
     }
     opA[d].release();
@@ -442,10 +473,10 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
         cur = cur_owner.u32();
       }
     }
-    if (stats) stats->postadd_ms = tpost.stop();
+    if (stats) tpost.stop(&stats->postadd_ms);
   }
   if (stats) {
-    stats->device_ms = total.stop();
+    total.stop(&stats->device_ms);
     stats->launches = launches;
     stats->depth = d;
   }
@@ -492,7 +523,7 @@ int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* l
     ++launches;
   }
   if (stats) {
-    stats->postadd_ms = tpost.stop();
+    tpost.stop(&stats->postadd_ms);
     stats->device_ms = stats->postadd_ms;
     stats->launches = launches;
     stats->depth = d;
@@ -767,6 +798,7 @@ int mpgpu_download(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t
 
 int mpgpu_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C,
                mpgpu_stats* stats) {
+  TimerGuard timer_guard;
   if (!h) return MPGPU_ERR_DOMAIN;
   int rc = validate_gemm(h, algo, param, A, B, C);
   if (rc) return rc;
@@ -793,6 +825,7 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
                     const uint32_t* al, const int32_t* ae, const uint8_t* as, const uint32_t* bl,
                     const int32_t* be, const uint8_t* bs, uint32_t* cl, int32_t* ce, uint8_t* cs, int32_t Lh,
                     mpgpu_stats* stats) {
+  TimerGuard timer_guard;
   // One stream-ordered sequence: pooled device buffers, H2D + layout conversion of A
   // and B, the product, conversion + D2H of C, and a single synchronisation.
   if (!h) return MPGPU_ERR_DOMAIN;
@@ -942,6 +975,7 @@ int mpgpu_fast_mul_trace(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_m
 
 int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min, int pivoting,
                      int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats) {
+  TimerGuard timer_guard;
   if (!h || !A) return MPGPU_ERR_DOMAIN;
   if (zero_pivot) *zero_pivot = 0;
   if (A->rows != A->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: matrix must be square");
@@ -1012,6 +1046,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
         count_fast_rec(kernel, rest, K, rest, n_min, c);
         stats->mul += c[0];
         stats->addsub += c[1];
+        flush_timers();  // ss is local: resolve its queued timings now
         stats->leaf_ms += ss.leaf_ms;
         stats->leaf_madds += ss.leaf_madds;
         stats->launches += ss.launches;
@@ -1021,7 +1056,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
     panel(off, n - off);
     return 0;
   });
-  if (stats) stats->device_ms = total.stop();
+  if (stats) total.stop(&stats->device_ms);
   if (rc) return rc;
   int64_t zpv = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&zpv, zp, sizeof zpv, cudaMemcpyDeviceToHost, h->stream));
@@ -1087,6 +1122,7 @@ int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out
 
 int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
                       int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products, mpgpu_stats* stats) {
+  TimerGuard timer_guard;
   if (!h || !A || !B || !node_products) return MPGPU_ERR_DOMAIN;
   if (A->cols != B->rows) return fail(h, MPGPU_ERR_DIMENSION, "inner dimension mismatch");
   if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
@@ -1108,6 +1144,7 @@ int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat*
 
 int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
                        const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats) {
+  TimerGuard timer_guard;
   if (!h || !C || !node_products) return MPGPU_ERR_DOMAIN;
   if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
   if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)

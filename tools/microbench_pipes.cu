@@ -96,6 +96,46 @@ __global__ void kmadd(uint32_t seed, uint32_t* out, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// mp_mul alone (short product + rounding) and mp_add alone, L limbs
+template <int L>
+__global__ void kmulonly(uint32_t seed, uint32_t* out, long long* cyc) {
+  mpg::MP<L> a, b, t;
+#pragma unroll
+  for (int i = 0; i < L; ++i) { a.m[i] = seed * (i + 7) + threadIdx.x; b.m[i] = seed ^ (i * 977 + threadIdx.x); }
+  a.m[L - 1] |= 0x80000000u; b.m[L - 1] |= 0x80000000u;
+  a.e = 0; b.e = 1; a.s = threadIdx.x & 1; b.s = 0;
+  __syncthreads();
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < 128; ++it) {
+    mpg::mp_mul<L>(a, b, 0, t);
+    b.m[0] ^= t.m[1];
+    b.m[L - 1] |= 0x80000000u;
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = b.m[0] ^ t.e;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int L>
+__global__ void kaddonly(uint32_t seed, uint32_t* out, long long* cyc) {
+  mpg::MP<L> acc, t;
+#pragma unroll
+  for (int i = 0; i < L; ++i) { acc.m[i] = seed * (i + 7) + threadIdx.x; t.m[i] = seed ^ (i * 977 + threadIdx.x); }
+  acc.m[L - 1] |= 0x80000000u; t.m[L - 1] |= 0x80000000u;
+  acc.e = 3; t.e = 1; acc.s = 0; t.s = threadIdx.x & 1;
+  __syncthreads();
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < 128; ++it) {
+    mpg::mp_add<L>(acc, t, 0u, 0, acc);
+    t.m[0] ^= acc.m[0];
+    t.s ^= acc.m[1] & 1u;
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc.m[0] ^ acc.e;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 template <class K>
 double run(K k, const char* name, double ops_per_thread_iter, int iters, int threads, int blocks_per_sm) {
   int sms = 0;
@@ -140,6 +180,8 @@ int main() {
   run(kmul<16>, "mul_full<16> (IMAD-eq 2L^2)", 2 * 16 * 16, 256, T, 2);
   run(kmul<32>, "mul_full<32> (IMAD-eq 2L^2)", 2 * 32 * 32, 256, 128, 2);
   run(kmadd<8>, "mp_mul+mp_add L=8 (IMAD-eq 2L^2)", 2 * 8 * 8, 128, T, B);
+  run(kmulonly<8>, "mp_mul only L=8 (IMAD-eq 2L^2)", 2 * 8 * 8, 128, T, B);
+  run(kaddonly<8>, "mp_add only L=8 (count 1 op = 128 'IMAD-eq')", 2 * 8 * 8, 128, T, B);
   run(kmadd<32>, "mp_mul+mp_add L=32 (IMAD-eq 2L^2)", 2 * 32 * 32, 128, 128, 2);
   return 0;
 }

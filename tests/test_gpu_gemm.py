@@ -170,3 +170,22 @@ def test_gemm_host_buffers_path(P, O, alg, param):
     want, ops = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
     assert P.identical(c, want)
     assert (st.mul, st.addsub) == ops
+
+
+@pytest.mark.gpu
+def test_randomized_shapes_precisions_algorithms(P, O):
+    # seeded sweep over shapes (incl. 1-wide and odd), precisions and cutoffs
+    rng = np.random.default_rng(20261020)
+    for _ in range(40):
+        m, l, n = (int(v) for v in rng.integers(1, 70, 3))
+        bits = int(rng.choice([2, 24, 33, 64, 97, 128, 160, 256, 300, 512, 700, 1024]))
+        alg = str(rng.choice(ALGS))
+        param = int(rng.integers(1, 20))
+        gen = [P.gen_uniform_full, P.gen_scaled, P.gen_random][int(rng.integers(0, 3))]
+        ctx = P.PrecisionContext(bits)
+        a, b = gen(m, l, int(rng.integers(1, 1 << 30)), ctx), gen(l, n, int(rng.integers(1, 1 << 30)), ctx)
+        ops = P.OpCounter()
+        c = _run(P, alg, param if alg != "simple" else 0, a, b, ctx, ops)
+        want, wops = O.gemm(alg, param if alg != "simple" else 0, O.OMat.of(a), O.OMat.of(b))
+        assert P.identical(c, want), (m, l, n, bits, alg, param)
+        assert (ops.mul, ops.addsub) == wops

@@ -194,6 +194,9 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 
 template <int L>
 void launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  if constexpr (L >= 8) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
+    if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
+  }
   constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
   constexpr int S = rec_stride(L);
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);

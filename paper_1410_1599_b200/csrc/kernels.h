@@ -26,6 +26,12 @@ struct GemmArgs {
 
 template <int L>
 void launch_gemm(const GemmArgs& g, cudaStream_t st);
+// tensor-core (tcgen05 kind::i8) variant of the same contract, L in {8, 16, 32};
+// returns false if it could not be configured (launch_gemm then uses the IMAD kernel)
+template <int L>
+bool launch_gemm_tc(const GemmArgs& g, cudaStream_t st);
+// MPGPU_GEMM=tc selects the tensor-core leaf (read once per process)
+bool gemm_tc_enabled();
 
 // SoA planes <-> records
 template <int L>

@@ -92,9 +92,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -181,27 +181,52 @@ __global__ void __launch_bounds__(Cfg<L>::NT, 1) gemm_tc_kernel(const GemmArgs g
       const uint32_t* s_bs = reinterpret_cast<const uint32_t*>(s_be + JT);
       const int32_t ea = s_ae[c_mine], eb = s_be[r_mine];
       const uint32_t sgn = s_as[c_mine] ^ s_bs[r_mine];
+      // Short combine: conv columns t >= C0 = 16(L/4 - 1) give the limbs L-4 .. 2L-1 of
+      // T = P - E with 0 <= E < 2^(32(L-4)+16) (the skipped columns), so the guard limb
+      // estimate is low by at most a carry.  Like mp_mul_g's short product: decide the
+      // rounding from T unless the guard limb is within reach of a boundary; then the
+      // whole warp re-reads all columns and combines the exact product.
+      constexpr int C0 = 4 * (L - 4);
       uint32_t P[2 * L];
-      uint32_t carry = 0;
       const uint32_t col0 = tbase + lane_base + (uint32_t)((b * SPB + sl) * NC);
+      auto combine = [&](int c16_begin) {
+        uint32_t carry = 0;
 #pragma unroll
-      for (int c16 = 0; c16 < NC / 16; ++c16) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(col0 + 16 * c16));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int c16 = 0; c16 < NC / 16; ++c16) {
+          if (c16 < c16_begin) continue;
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(col0 + 16 * c16));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          // limb = D[4q] + D[4q+1] 2^8 + D[4q+2] 2^16 + D[4q+3] 2^24 + carry   (exact)
-          const uint32_t x = v[4 * qq + 1] * 256u + v[4 * qq] + carry;  // < 2^32
-          const uint32_t y = v[4 * qq + 3] * 256u + v[4 * qq + 2];      // < 2^31
-          const uint64_t w = (uint64_t)y * 65536u + x;
-          P[4 * c16 + qq] = (uint32_t)w;
-          carry = (uint32_t)(w >> 32);
+          for (int qq = 0; qq < 4; ++qq) {
+            // limb = D[4q] + D[4q+1] 2^8 + D[4q+2] 2^16 + D[4q+3] 2^24 + carry   (exact)
+            const uint32_t x = v[4 * qq + 1] * 256u + v[4 * qq] + carry;  // < 2^32
+            const uint32_t y = v[4 * qq + 3] * 256u + v[4 * qq + 2];      // < 2^31
+            const uint64_t w = (uint64_t)y * 65536u + x;
+            P[4 * c16 + qq] = (uint32_t)w;
+            carry = (uint32_t)(w >> 32);
+          }
         }
+      };
+      combine(C0 / 16);
+      const bool nonzero = ea != EXP_ZERO && eb != EXP_ZERO;
+      uint32_t s1 = (P[2 * L - 1] >> 31) ^ 1u;
+      uint32_t gd = __funnelshift_l(P[L - 2], P[L - 1], s1);
+      constexpr uint32_t MARGIN = 64u;
+      const bool decided = (g.sh == 0) ? (gd < 0x80000000u - MARGIN || (gd > 0x80000000u && gd < 0xFFFFFFFFu - MARGIN))
+                                       : (gd != 0u && gd < 0xFFFFFFFFu - MARGIN);
+      uint32_t stk = 1u;  // decided: the rest below the guard limb is nonzero or irrelevant
+      if (__any_sync(0xFFFFFFFFu, active && nonzero && !decided)) {
+        combine(0);
+        s1 = (P[2 * L - 1] >> 31) ^ 1u;
+        gd = __funnelshift_l(P[L - 2], P[L - 1], s1);
+        stk = P[L - 2] << s1;
+#pragma unroll
+        for (int kk = 0; kk < L - 2; ++kk) stk |= P[kk];
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
@@ -211,18 +236,13 @@ __global__ void __launch_bounds__(Cfg<L>::NT, 1) gemm_tc_kernel(const GemmArgs g
       }
       if (active) {
         MP<L> t;
-        if (ea == EXP_ZERO || eb == EXP_ZERO) {
+        if (!nonzero) {
           mp_zero(t, sgn);
         } else {
           t.s = sgn;
-          const uint32_t s1 = (P[2 * L - 1] >> 31) ^ 1u;
           int32_t e = ea + eb - (int32_t)s1;
 #pragma unroll
           for (int kk = 0; kk < L; ++kk) t.m[kk] = __funnelshift_l(P[L + kk - 1], P[L + kk], s1);
-          const uint32_t gd = __funnelshift_l(P[L - 2], P[L - 1], s1);
-          uint32_t stk = P[L - 2] << s1;
-#pragma unroll
-          for (int kk = 0; kk < L - 2; ++kk) stk |= P[kk];
           round_p<L>(t.m, gd, stk, g.sh, e);
           t.e = e;
         }

@@ -41,9 +41,14 @@ extern "C" {
 #define MPGPU_ERR_SINGULAR 3  /* mpmm::SingularError   (errors.hpp:26-31), pivot index out-param */
 #define MPGPU_ERR_CUDA 4      /* device / runtime failure (no reference analogue) */
 #define MPGPU_ERR_NOMEM 5     /* device allocation failed */
+#define MPGPU_ERR_UNDEFINED_METRIC 6 /* mpmm::UndefinedMetricError (errors.hpp:41-43) */
 
 #define MPGPU_EXP_ZERO INT32_MIN
-#define MPGPU_MAX_PREC 1024 /* largest precision with a device kernel (32 limbs) */
+#define MPGPU_MAX_PREC 1024 /* largest precision of the arithmetic entry points (32 limbs) */
+/* Matrices may be allocated, uploaded and downloaded up to MPGPU_MAX_STORE_PREC (64
+ * limbs) -- the double-precision references of the accuracy metrics; every other
+ * entry point rejects them with DOMAIN. */
+#define MPGPU_MAX_STORE_PREC 2048
 
 /* mpmm::Algorithm (fastmm.hpp:13) */
 enum { MPGPU_SIMPLE = 0, MPGPU_BLOCK = 1, MPGPU_STRASSEN = 2, MPGPU_WINOGRAD = 3 };
@@ -85,7 +90,7 @@ int mpgpu_synchronize(mpgpu_handle* h);
 /* device-to-device copy on the handle's stream (raw record buffers) */
 int mpgpu_copy_device(mpgpu_handle* h, void* dst, const void* src, size_t bytes);
 
-/* device limb count used for a precision (0 if prec is outside [2, MPGPU_MAX_PREC]) */
+/* device limb count used for a precision (0 if prec is outside [2, MPGPU_MAX_STORE_PREC]) */
 int mpgpu_nlimbs_for(int32_t prec);
 int mpgpu_record_words(int32_t nlimbs);
 
@@ -149,6 +154,28 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
  * the LU tolerance). */
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b,
                    mpgpu_mat* x, int exact, int64_t* zero_pivot);
+
+/* ---- accuracy metrics (device-side; bench.hpp:145-147, 217, 238) ---------
+ * Results are returned as host SoA scalars at the reference's precision, limb planes
+ * of nlimbs_out = ref->nlimbs limbs (limbs[k * count + e] is limb k of result e).
+ *
+ * max_rel_error (matrix.hpp:253-279): out {max, min} of rel_error(approx, ref) =
+ * RN(|RN(approx - ref)| / |ref|) at ref->prec (precision.hpp:187-193) over the
+ * elements with ref != 0; *skipped = count of zero references.  approx->prec <=
+ * ref->prec (the approximation is widened exactly).  Shape mismatch -> DIMENSION;
+ * all references zero -> UNDEFINED_METRIC. */
+int mpgpu_max_rel_error(mpgpu_handle* h, const mpgpu_mat* approx, const mpgpu_mat* ref, uint32_t* out_limbs,
+                        int32_t* out_exp, uint8_t* out_sign, int64_t* skipped);
+/* max_rel_error_solution (blocklu.hpp:306-333) for n x 1 vectors at one precision:
+ * out {max_rel over xtrue != 0, max |xhat - xtrue| over xtrue == 0 (+0 if none)};
+ * *zero_refs = number of zero components.  Length mismatch -> DIMENSION; every
+ * component zero -> UNDEFINED_METRIC. */
+int mpgpu_solution_error(mpgpu_handle* h, const mpgpu_mat* xhat, const mpgpu_mat* xtrue, uint32_t* out_limbs,
+                         int32_t* out_exp, uint8_t* out_sign, int64_t* zero_refs);
+/* one_norm (matrix.hpp:237-251): max over columns of the top-to-bottom RN sum of |a_ij|
+ * at A->prec; out: one scalar. */
+int mpgpu_one_norm(mpgpu_handle* h, const mpgpu_mat* A, uint32_t* out_limbs, int32_t* out_exp,
+                   uint8_t* out_sign);
 
 /* ---- multi-GPU building blocks -------------------------------------------
  * A strided window of a device matrix (no copy; not owned). */

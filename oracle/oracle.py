@@ -333,3 +333,69 @@ def to_double(x):
     out = np.zeros(n, np.float64)
     orc().orc_to_double(C.c_long(x.bits()), x.nlimbs, C.c_int64(n), *_soa(x), _p(out))
     return out.reshape(x.rows(), x.cols())
+
+
+# ---- accuracy metrics and benchmark drivers (compiled reference) -------------
+
+def max_rel_error(approx, ref_m):
+    """matrix.hpp:260-279 -> (OMat 2x1 {max, min} at ref's precision, skipped)."""
+    n = ref_m.rows() * ref_m.cols()
+    out = OMat(2, 1, ref_m.bits())
+    sk = C.c_int64(0)
+    _check(ref().ref_max_rel_error(C.c_long(approx.bits()), approx.nlimbs, C.c_long(ref_m.bits()), ref_m.nlimbs,
+                                   C.c_int64(ref_m.rows()), C.c_int64(ref_m.cols()), *_soa(approx), *_soa(ref_m),
+                                   *_soa(out), C.byref(sk)))
+    return out, int(sk.value)
+
+
+def solution_error(xhat, xtrue):
+    """blocklu.hpp:312-333 -> (OMat 2x1 {max_rel, max_zero_abs}, zero_refs)."""
+    n = xtrue.rows() * xtrue.cols()
+    out = OMat(2, 1, xtrue.bits())
+    zr = C.c_int64(0)
+    _check(ref().ref_solution_error(C.c_long(xtrue.bits()), xtrue.nlimbs, C.c_int64(n), *_soa(xhat),
+                                    *_soa(xtrue), *_soa(out), C.byref(zr)))
+    return out, int(zr.value)
+
+
+def one_norm(a):
+    out = OMat(1, 1, a.bits())
+    _check(ref().ref_one_norm(C.c_long(a.bits()), a.nlimbs, C.c_int64(a.rows()), C.c_int64(a.cols()), *_soa(a),
+                              *_soa(out)))
+    return out
+
+
+def gen_lotkin(n, bits):
+    x = OMat(n, n, bits)
+    _check(ref().ref_gen_lotkin(C.c_int64(n), C.c_long(bits), x.nlimbs, *_soa(x)))
+    return x
+
+
+def to_decimal(x, digits):
+    n = x.rows() * x.cols()
+    buf = C.create_string_buffer(n * (digits + 32) + 64)
+    _check(ref().ref_to_decimal(C.c_long(x.bits()), x.nlimbs, C.c_int64(n), *_soa(x), C.c_int(digits), buf,
+                                C.c_int64(len(buf))))
+    return buf.value.decode().split("\n")
+
+
+def run_matmul(m, l, n, bits, n_min, algos=("simple", "block", "strassen", "winograd"), ref_mult=2,
+               verbose=False):
+    """bench.hpp:117-165 -> CSV text (print_csv)."""
+    mask = 0
+    for a in algos:
+        mask |= 1 << _algo(a)
+    buf = C.create_string_buffer(1 << 20)
+    _check(ref().ref_run_matmul(C.c_int64(m), C.c_int64(l), C.c_int64(n), C.c_long(bits), C.c_int64(n_min), mask,
+                                C.c_long(ref_mult), int(verbose), buf, C.c_int64(len(buf))))
+    return buf.value.decode()
+
+
+def run_lu(kind, n, bits, kernel, n_min, alpha_lo, alpha_hi, seed=1, verbose=False):
+    """bench.hpp:187-249 -> (CSV text, any_singular)."""
+    buf = C.create_string_buffer(1 << 20)
+    s = C.c_int(0)
+    _check(ref().ref_run_lu(0 if kind == "random" else 1, C.c_int64(n), C.c_long(bits), _algo(kernel),
+                            C.c_int64(n_min), C.c_int64(alpha_lo), C.c_int64(alpha_hi), C.c_uint64(seed),
+                            int(verbose), buf, C.c_int64(len(buf)), C.byref(s)))
+    return buf.value.decode(), bool(s.value)

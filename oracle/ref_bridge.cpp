@@ -7,11 +7,13 @@
 // TEST INFRASTRUCTURE ONLY (the checker, and the --impl reference CPU arm of
 // bench.py).  Matrices cross this boundary in the C-ABI's SoA format
 // (oracle/soa_mpfr.h).  Return codes: 0 ok, 1 DimensionError, 2 DomainError,
-// 3 SingularError (pivot index via out-param), 4 other mpmm::Error, 5 internal.
+// 3 SingularError (pivot index via out-param), 4 other mpmm::Error, 5 internal,
+// 6 UndefinedMetricError.
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -57,6 +59,8 @@ int guarded(F&& f, std::int64_t* pivot = nullptr) {
     return 1;
   } catch (const DomainError&) {
     return 2;
+  } catch (const UndefinedMetricError&) {
+    return 6;
   } catch (const Error&) {
     return 4;
   } catch (...) {
@@ -353,6 +357,127 @@ int ref_recursion_plan(std::int64_t m, std::int64_t l, std::int64_t n, std::int6
       r[7] = plan[i].base ? 1 : 0;
     }
     return 0;
+  });
+}
+
+// ---- accuracy metrics and benchmark drivers (matrix.hpp:237-279, blocklu.hpp:306-333,
+// bench.hpp:117-249) -- checkers of the device metrics and of the GPU CSV rows.
+int ref_max_rel_error(long pa, int La, long pr, int Lr, std::int64_t rows, std::int64_t cols,
+                      const std::uint32_t* al, const std::int32_t* ae, const std::uint8_t* as,
+                      const std::uint32_t* rl, const std::int32_t* re, const std::uint8_t* rs,
+                      std::uint32_t* ol, std::int32_t* oe, std::uint8_t* os, std::int64_t* skipped) {
+  return guarded([&] {
+    Matrix a = load(rows, cols, pa, La, al, ae, as);
+    Matrix r = load(rows, cols, pr, Lr, rl, re, rs);
+    RelErrorStats st = max_rel_error(a, r);
+    Matrix out(2, 1, PrecisionContext(pr));
+    out.at(0, 0) = st.max;
+    out.at(1, 0) = st.min;
+    *skipped = static_cast<std::int64_t>(st.skipped_zero_refs);
+    return store(out, Lr, ol, oe, os);
+  });
+}
+
+int ref_solution_error(long prec, int L, std::int64_t n, const std::uint32_t* xl, const std::int32_t* xe,
+                       const std::uint8_t* xs, const std::uint32_t* tl, const std::int32_t* te,
+                       const std::uint8_t* ts, std::uint32_t* ol, std::int32_t* oe, std::uint8_t* os,
+                       std::int64_t* zero_refs) {
+  return guarded([&] {
+    Matrix x = load(n, 1, prec, L, xl, xe, xs), t = load(n, 1, prec, L, tl, te, ts);
+    Vector xv, tv;
+    for (std::int64_t i = 0; i < n; ++i) {
+      xv.push_back(x.at(i, 0));
+      tv.push_back(t.at(i, 0));
+    }
+    SolutionError se = max_rel_error_solution(xv, tv);
+    Matrix out(2, 1, PrecisionContext(prec));
+    out.at(0, 0) = se.max_rel;
+    out.at(1, 0) = se.max_zero_abs;
+    *zero_refs = static_cast<std::int64_t>(se.zero_refs);
+    return store(out, L, ol, oe, os);
+  });
+}
+
+int ref_one_norm(long prec, int L, std::int64_t rows, std::int64_t cols, const std::uint32_t* al,
+                 const std::int32_t* ae, const std::uint8_t* as, std::uint32_t* ol, std::int32_t* oe,
+                 std::uint8_t* os) {
+  return guarded([&] {
+    Matrix a = load(rows, cols, prec, L, al, ae, as);
+    Matrix out(1, 1, PrecisionContext(prec));
+    out.at(0, 0) = one_norm(a);
+    return store(out, L, ol, oe, os);
+  });
+}
+
+// gen_lotkin (matgen.hpp:107-121)
+int ref_gen_lotkin(std::int64_t n, long prec, int L, std::uint32_t* xl, std::int32_t* xe, std::uint8_t* xs) {
+  return guarded([&] { return store(gen_lotkin(n, PrecisionContext(prec)), L, xl, xe, xs); });
+}
+
+// to_decimal (precision.hpp:293-300) of N elements, '\n'-joined into buf
+int ref_to_decimal(long prec, int L, std::int64_t N, const std::uint32_t* xl, const std::int32_t* xe,
+                   const std::uint8_t* xs, int digits, char* buf, std::int64_t buflen) {
+  return guarded([&] {
+    Matrix m = load(N, 1, prec, L, xl, xe, xs);
+    std::string out;
+    for (std::int64_t i = 0; i < N; ++i) {
+      if (i) out += '\n';
+      out += to_decimal(m.at(i, 0), digits);
+    }
+    if (static_cast<std::int64_t>(out.size()) + 1 > buflen) return 1;
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+    return 0;
+  });
+}
+
+namespace {
+int csv_out(const std::vector<BenchRecord>& rows, char* buf, std::int64_t buflen) {
+  std::ostringstream os;
+  print_csv(os, rows);
+  const std::string s = os.str();
+  if (static_cast<std::int64_t>(s.size()) + 1 > buflen) return 1;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+}  // namespace
+
+// run_matmul (bench.hpp:117-165): algo_mask bit a selects Algorithm a
+int ref_run_matmul(std::int64_t m, std::int64_t l, std::int64_t n, long bits, std::int64_t n_min, int algo_mask,
+                   long ref_mult, int verbose, char* buf, std::int64_t buflen) {
+  return guarded([&] {
+    MatmulRequest q;
+    q.algos.clear();
+    for (int a = 0; a < 4; ++a)
+      if (algo_mask & (1 << a)) q.algos.push_back(algo_of(a));
+    q.m = m;
+    q.l = l;
+    q.n = n;
+    q.bits = bits;
+    q.n_min = n_min;
+    q.ref_bits_multiplier = ref_mult;
+    q.verbose = verbose != 0;
+    return csv_out(run_matmul(q), buf, buflen);
+  });
+}
+
+// run_lu (bench.hpp:187-249): kind 0 random, 1 lotkin
+int ref_run_lu(int kind, std::int64_t n, long bits, int kernel, std::int64_t n_min, std::int64_t alo,
+               std::int64_t ahi, std::uint64_t seed, int verbose, char* buf, std::int64_t buflen,
+               int* any_singular) {
+  return guarded([&] {
+    LURequest q;
+    q.matrix_kind = kind == 0 ? "random" : "lotkin";
+    q.n = n;
+    q.bits = bits;
+    q.kernel = algo_of(kernel);
+    q.n_min = n_min;
+    q.alpha_lo = alo;
+    q.alpha_hi = ahi;
+    q.seed = seed;
+    q.verbose = verbose != 0;
+    LUOutcome o = run_lu(q);
+    *any_singular = o.any_singular ? 1 : 0;
+    return csv_out(o.rows, buf, buflen);
   });
 }
 

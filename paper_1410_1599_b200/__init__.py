@@ -7,7 +7,10 @@ from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix
                    block_mul, count_fast, count_simple, equal_values, fast_mul, gemm_host, gemm_into, handle, identical,
                    lu_blocked, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
                    record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
-                   solve_columnwise, sub, vec_op)
+                   solve_columnwise, sub, vec_op, UndefinedMetricError, RelErrorStats, SolutionError,
+                   max_rel_error, max_rel_error_solution, one_norm)
 from .matgen import Prng64, from_ints, gen_random, gen_scaled, gen_uniform_full, to_fractions
+from .benchdrv import (CSV_HEADER, BenchRecord, LUOutcome, LURequest, MatmulRequest, append_csv, bench_reference,
+                       gen_bench_pair, gen_linear_system, gen_lotkin, print_csv, run_lu, run_matmul)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -18,7 +18,7 @@ BUILD = PKG / "_build"
 LIB = PKG / "libmpgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["gemm.cu", "gemm_tc.cu", "elementwise.cu", "lu.cu", "capi.cu"]
+SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu"]
 HEADERS = ["mp_arith.cuh", "kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",

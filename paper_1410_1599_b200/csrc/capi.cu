@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -53,10 +54,10 @@ int fail(mpgpu_handle* h, int code, const char* fmt, ...) {
                   "%s: %s", #expr, cudaGetErrorString(e_));                                 \
   } while (0)
 
-constexpr int kLimbOptions[] = {1, 2, 4, 8, 16, 32};
+constexpr int kLimbOptions[] = {1, 2, 4, 8, 16, 32, 64};  // 64: storage / metrics only
 
 int nlimbs_for(int32_t prec) {
-  if (prec < 2 || prec > MPGPU_MAX_PREC) return 0;
+  if (prec < 2 || prec > MPGPU_MAX_STORE_PREC) return 0;
   const int need = (prec + 31) / 32;
   for (int L : kLimbOptions)
     if (L >= need) return L;
@@ -74,6 +75,13 @@ int dispatch_L(int L, F&& f) {
     case 32: return f(std::integral_constant<int, 32>{});
     default: return MPGPU_ERR_DOMAIN;
   }
+}
+
+// storage-level dispatch (record conversion, accuracy metrics): also 64 limbs
+template <class F>
+int dispatch_store(int L, F&& f) {
+  if (L == 64) return f(std::integral_constant<int, 64>{});
+  return dispatch_L(L, std::forward<F>(f));
 }
 
 // RAII device scratch on the handle's stream (stream-ordered pool allocator)
@@ -531,6 +539,15 @@ int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* l
   return MPGPU_OK;
 }
 
+// arithmetic entry points: 64-limb (p > 1024) matrices are storage / metrics only
+int compute_range(mpgpu_handle* h, std::initializer_list<const mpgpu_mat*> ms) {
+  for (const mpgpu_mat* m : ms)
+    if (m && m->nlimbs > 32)
+      return fail(h, MPGPU_ERR_DOMAIN, "precision %d above %d bits: storage and accuracy metrics only", m->prec,
+                  MPGPU_MAX_PREC);
+  return MPGPU_OK;
+}
+
 int validate_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B,
                   const mpgpu_mat* C) {
   if (!A || !B || !C) return fail(h, MPGPU_ERR_DIMENSION, "null matrix");
@@ -545,7 +562,7 @@ int validate_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, 
     return fail(h, MPGPU_ERR_DIMENSION, "output shape mismatch");
   if (A->prec != C->prec || B->prec != C->prec || A->nlimbs != C->nlimbs || B->nlimbs != C->nlimbs)
     return fail(h, MPGPU_ERR_DOMAIN, "device GEMM requires one precision for A, B and C");
-  return MPGPU_OK;
+  return compute_range(h, {A, B, C});
 }
 
 // ---- host generators -----------------------------------------------------
@@ -626,7 +643,7 @@ int upload_async(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_
   }
   CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, h->stream));
-  dispatch_L(L, [&](auto Lc) {
+  dispatch_store(L, [&](auto Lc) {
     mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, rec, h->stream);
     return 0;
   });
@@ -640,7 +657,7 @@ int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint3
   uint32_t* dl = stage.u32();
   int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
   uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
-  dispatch_L(L, [&](auto Lc) {
+  dispatch_store(L, [&](auto Lc) {
     mpg::launch_rec2soa<decltype(Lc)::value>(rec, N, dl, de, ds, N, h->stream);
     return 0;
   });
@@ -830,7 +847,8 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
   // and B, the product, conversion + D2H of C, and a single synchronisation.
   if (!h) return MPGPU_ERR_DOMAIN;
   const int L = nlimbs_for(prec);
-  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
+  if (!L || L > 32)
+    return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
   if (m < 1 || l < 1 || n < 1) return fail(h, MPGPU_ERR_DIMENSION, "matrix dimensions must be at least 1x1");
   if (Lh < (prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   mpgpu_mat A{m, l, prec, L, nullptr, l, 0}, B{l, n, prec, L, nullptr, n, 0}, C{m, n, prec, L, nullptr, n, 0};
@@ -871,6 +889,7 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
 
 int mpgpu_addsub(mpgpu_handle* h, int is_sub, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C) {
   if (!h || !A || !B || !C) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {A, B, C})) return r;
   if (A->prec != B->prec) return fail(h, MPGPU_ERR_DOMAIN, is_sub ? "mat sub: mixed precisions" : "mat add: mixed precisions");
   if (A->rows != B->rows || A->cols != B->cols || C->rows != A->rows || C->cols != A->cols)
     return fail(h, MPGPU_ERR_DIMENSION, "shape mismatch: %lldx%lld vs %lldx%lld", (long long)A->rows,
@@ -891,6 +910,7 @@ int mpgpu_addsub(mpgpu_handle* h, int is_sub, const mpgpu_mat* A, const mpgpu_ma
 
 int mpgpu_vec_op(mpgpu_handle* h, int op, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C) {
   if (!h || !A || !B || !C) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {A, B, C})) return r;
   if (A->rows * A->cols != B->rows * B->cols || C->rows * C->cols != A->rows * A->cols)
     return fail(h, MPGPU_ERR_DIMENSION, "vec_op: size mismatch");
   if (A->prec != C->prec || B->prec != C->prec) return fail(h, MPGPU_ERR_DOMAIN, "vec_op: mixed precisions");
@@ -978,6 +998,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
   TimerGuard timer_guard;
   if (!h || !A) return MPGPU_ERR_DOMAIN;
   if (zero_pivot) *zero_pivot = 0;
+  if (int r = compute_range(h, {A})) return r;
   if (A->rows != A->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: matrix must be square");
   if (K == 0) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: block size must be at least 1");
   if (A->ld != A->cols) return fail(h, MPGPU_ERR_DOMAIN, "lu_blocked: dense matrix required");
@@ -1074,6 +1095,7 @@ int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, cons
                    int exact, int64_t* zero_pivot) {
   if (!h || !F || !b || !x) return MPGPU_ERR_DOMAIN;
   if (zero_pivot) *zero_pivot = 0;
+  if (int r = compute_range(h, {F, b, x})) return r;
   const int64_t n = F->rows;
   if (F->rows != F->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: factors must be square");
   if (b->rows * b->cols != n || x->rows * x->cols != n) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: length mismatch");
@@ -1124,6 +1146,7 @@ int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat*
                       int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products, mpgpu_stats* stats) {
   TimerGuard timer_guard;
   if (!h || !A || !B || !node_products) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {A, B})) return r;
   if (A->cols != B->rows) return fail(h, MPGPU_ERR_DIMENSION, "inner dimension mismatch");
   if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
   if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
@@ -1146,6 +1169,7 @@ int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int 
                        const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats) {
   TimerGuard timer_guard;
   if (!h || !C || !node_products) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {C})) return r;
   if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
   if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
     return fail(h, MPGPU_ERR_DOMAIN, "fast_mul: algorithm must be strassen or winograd");
@@ -1160,6 +1184,104 @@ int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int 
   });
   if (rc) return rc;
   return check_err(h);
+}
+
+// ---- accuracy metrics (metrics.cu) -------------------------------------------
+namespace {
+// elementwise metric kernel + reduction, then the three result records -> host SoA
+// (count = how many of them the caller wants: 2 or 1)
+int run_metric(mpgpu_handle* h, int mode, const mpgpu_mat* approx, const mpgpu_mat* ref, int count, int which0,
+               int which1, uint32_t* ol, int32_t* oe, uint8_t* os, int64_t* counted, bool* empty_a) {
+  const int L = ref->nlimbs;
+  const int64_t N = ref->rows * ref->cols;
+  const int S = rec_stride(L);
+  DevBuf bufA, bufB, scratch, out3, cnt, soa;
+  CUDA_TRY(h, bufA.alloc(h, sizeof(uint32_t) * S * N));
+  if (mode == 1) CUDA_TRY(h, bufB.alloc(h, sizeof(uint32_t) * S * N));
+  CUDA_TRY(h, scratch.alloc(h, sizeof(uint32_t) * S * 3 * 1024));
+  CUDA_TRY(h, out3.alloc(h, sizeof(uint32_t) * S * 3));
+  CUDA_TRY(h, cnt.alloc(h, sizeof(unsigned long long)));
+  CUDA_TRY(h, cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * L - ref->prec;
+  int rc = dispatch_store(L, [&](auto Lc) {
+    constexpr int LL = decltype(Lc)::value;
+    if (mode == 2) {
+      mpg::launch_colsum_abs<LL>(ref->rec, ref->ld, (int)ref->rows, (int)ref->cols, sh, bufA.u32(), h->d_err,
+                                 h->stream);
+      mpg::launch_reduce3<LL>(bufA.u32(), nullptr, ref->cols, out3.u32(), scratch.u32(), h->stream);
+    } else {
+      mpg::launch_rel_error<LL>(approx->rec, approx->nlimbs, approx->ld, ref->rec, ref->ld, (int)ref->rows,
+                                (int)ref->cols, mode, sh, bufA.u32(), mode == 1 ? bufB.u32() : nullptr,
+                                static_cast<unsigned long long*>(cnt.p), h->d_err, h->stream);
+      mpg::launch_reduce3<LL>(bufA.u32(), mode == 1 ? bufB.u32() : nullptr, N, out3.u32(), scratch.u32(),
+                              h->stream);
+    }
+    return 0;
+  });
+  if (rc) return fail(h, MPGPU_ERR_DOMAIN, "metric: unsupported limb count %d", L);
+  // read back the three records and the counter
+  std::vector<uint32_t> host(3 * S);
+  unsigned long long c = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(host.data(), out3.p, sizeof(uint32_t) * 3 * S, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(&c, cnt.p, sizeof c, cudaMemcpyDeviceToHost, h->stream));
+  rc = check_err(h);
+  if (rc) return rc;
+  if (counted) *counted = (int64_t)c;
+  *empty_a = (host[L + 1] & 2u) != 0;
+  const int which[2] = {which0, which1};
+  for (int e = 0; e < count; ++e) {
+    const uint32_t* r = host.data() + which[e] * S;
+    const bool skip = (r[L + 1] & 2u) != 0;  // empty set: +0
+    for (int k = 0; k < L; ++k) ol[(size_t)k * count + e] = skip ? 0u : r[k];
+    oe[e] = skip ? MPGPU_EXP_ZERO : (int32_t)r[L];
+    os[e] = skip ? 0 : (uint8_t)(r[L + 1] & 1u);
+  }
+  return MPGPU_OK;
+}
+}  // namespace
+
+int mpgpu_max_rel_error(mpgpu_handle* h, const mpgpu_mat* approx, const mpgpu_mat* ref, uint32_t* ol, int32_t* oe,
+                        uint8_t* os, int64_t* skipped) {
+  if (!h || !approx || !ref || !ol || !oe || !os) return MPGPU_ERR_DOMAIN;
+  if (approx->rows != ref->rows || approx->cols != ref->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "shape mismatch: %lldx%lld vs %lldx%lld", (long long)approx->rows,
+                (long long)approx->cols, (long long)ref->rows, (long long)ref->cols);
+  if (approx->nlimbs > ref->nlimbs)
+    return fail(h, MPGPU_ERR_DOMAIN, "max_rel_error: the approximation is wider than the reference");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  bool empty = false;
+  int rc = run_metric(h, 0, approx, ref, 2, 0, 1, ol, oe, os, skipped, &empty);
+  if (rc) return rc;
+  if (empty) return fail(h, MPGPU_ERR_UNDEFINED_METRIC, "max_rel_error: all reference entries are zero");
+  return MPGPU_OK;
+}
+
+int mpgpu_solution_error(mpgpu_handle* h, const mpgpu_mat* xhat, const mpgpu_mat* xtrue, uint32_t* ol, int32_t* oe,
+                         uint8_t* os, int64_t* zero_refs) {
+  if (!h || !xhat || !xtrue || !ol || !oe || !os) return MPGPU_ERR_DOMAIN;
+  if (xhat->rows * xhat->cols != xtrue->rows * xtrue->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "solution error: length mismatch");
+  if (xhat->cols != 1 || xtrue->cols != 1)
+    return fail(h, MPGPU_ERR_DIMENSION, "solution error: vectors are n x 1 matrices");
+  if (xhat->nlimbs > xtrue->nlimbs)
+    return fail(h, MPGPU_ERR_DOMAIN, "solution error: the solution is wider than the reference");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  bool empty = false;
+  int rc = run_metric(h, 1, xhat, xtrue, 2, 0, 2, ol, oe, os, zero_refs, &empty);
+  if (rc) return rc;
+  if (empty) return fail(h, MPGPU_ERR_UNDEFINED_METRIC, "solution error: all reference components are zero");
+  return MPGPU_OK;
+}
+
+int mpgpu_one_norm(mpgpu_handle* h, const mpgpu_mat* A, uint32_t* ol, int32_t* oe, uint8_t* os) {
+  if (!h || !A || !ol || !oe || !os) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  bool empty = false;
+  return run_metric(h, 2, nullptr, A, 1, 0, 0, ol, oe, os, nullptr, &empty);
 }
 
 int mpgpu_matrix_view(const mpgpu_mat* parent, int64_t r0, int64_t c0, int64_t rows, int64_t cols, mpgpu_mat* out) {
@@ -1210,7 +1332,7 @@ int mpgpu_recursion_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t
 
 int mpgpu_gen(int kind, int64_t N, uint64_t seed, int32_t prec, uint32_t* limbs, int32_t* exp, uint8_t* sign,
               int32_t Lh) {
-  if (prec < 2 || Lh < (prec + 31) / 32) return MPGPU_ERR_DOMAIN;
+  if (prec < 2 || prec > MPGPU_MAX_STORE_PREC || Lh < (prec + 31) / 32) return MPGPU_ERR_DOMAIN;
   Prng64 rng(seed);
   for (int64_t e = 0; e < N; ++e) {
     if (kind == 0) {

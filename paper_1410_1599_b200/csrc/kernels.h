@@ -113,4 +113,24 @@ template <int L>
 void launch_sub2d(uint32_t* C, int64_t ldc, const uint32_t* T, int rows, int cols, int sh,
                   uint32_t* err, cudaStream_t st);
 
+// ---- accuracy metrics (metrics.cu), L in {1..32, 64} -----------------------
+// mode 0: outA[t] = rel_error(approx, ref) = RN(|RN(approx - ref)| / |ref|) at the
+//         reference precision (precision.hpp:187-193), SKIP-flagged and counted where
+//         ref == 0 (matrix.hpp:253-279); approx has la <= L limbs, widened exactly.
+// mode 1: solution error (blocklu.hpp:312-333): as mode 0 for nonzero refs; zero refs
+//         give outB[t] = RN(|approx - ref|) and are counted.
+template <int L>
+void launch_rel_error(const uint32_t* approx, int la, int64_t lda, const uint32_t* ref, int64_t ldr, int rows,
+                      int cols, int mode, int sh, uint32_t* outA, uint32_t* outB, unsigned long long* counter,
+                      uint32_t* err, cudaStream_t st);
+// one_norm column sums (matrix.hpp:237-251): out[j] = RN sum of |a_ij|, i ascending
+template <int L>
+void launch_colsum_abs(const uint32_t* A, int64_t ld, int rows, int cols, int sh, uint32_t* out, uint32_t* err,
+                       cudaStream_t st);
+// (max A, min A, max B) over N flagged nonnegative records -> 3 records (flag bit 1 of the
+// sign word set when a set was empty); scratch: 3 * 1024 records
+template <int L>
+void launch_reduce3(const uint32_t* A, const uint32_t* B, int64_t N, uint32_t* out3, uint32_t* scratch,
+                    cudaStream_t st);
+
 }  // namespace mpg

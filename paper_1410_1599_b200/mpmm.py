@@ -65,6 +65,10 @@ class SingularError(Error):
         self.pivot_index = pivot_index
 
 
+class UndefinedMetricError(Error):
+    """mpmm::UndefinedMetricError (errors.hpp:41-43)"""
+
+
 class DeviceError(Error):
     """CUDA / allocation failure (no reference analogue)."""
 
@@ -79,6 +83,8 @@ def _raise(h, rc: int, pivot: int = 0):
         raise DomainError(msg)
     if rc == 3:
         raise SingularError(msg, pivot)
+    if rc == 6:
+        raise UndefinedMetricError(msg)
     raise DeviceError(f"[{rc}] {msg}")
 
 
@@ -88,8 +94,9 @@ def _raise(h, rc: int, pivot: int = 0):
 
 
 class PrecisionContext:
-    """precision.hpp:18-36 -- p in [2, 2^20]; RNDN fixed.  The device path
-    supports p <= 1024 (mpgpu.h MPGPU_MAX_PREC)."""
+    """precision.hpp:18-36 -- p in [2, 2^20]; RNDN fixed.  The device arithmetic
+    supports p <= 1024 (mpgpu.h MPGPU_MAX_PREC); device matrices up to 2048 bits
+    (MPGPU_MAX_STORE_PREC) hold the references of the accuracy metrics."""
 
     min_bits = 2
     max_bits = 1 << 20
@@ -750,3 +757,96 @@ def solve(a: Matrix, b: Matrix, cfg: BlockLUConfig, ctx: PrecisionContext, pivot
 def solve_columnwise(a: Matrix, b: Matrix) -> Matrix:
     """blocklu.hpp:256-259"""
     return lu_solve(lu_columnwise(a), b, a.ctx())
+
+
+# ---------------------------------------------------------------------------
+# accuracy metrics, device-side (matrix.hpp:237-279, blocklu.hpp:306-333)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class RelErrorStats:
+    """matrix.hpp:253-258; max / min are 1x1 Matrices at the reference's precision."""
+    max: Matrix
+    min: Matrix
+    skipped_zero_refs: int = 0
+
+
+@dataclass
+class SolutionError:
+    """blocklu.hpp:306-310"""
+    max_rel: Matrix
+    max_zero_abs: Matrix
+    zero_refs: int = 0
+
+
+def _dev(x, ctx=None):
+    if isinstance(x, DeviceMatrix):
+        return x, False
+    return x.to_device(), True
+
+
+def _metric_out(ref_bits: int, count: int):
+    L = nlimbs_for(ref_bits)
+    return (np.zeros((L, count), np.uint32), np.zeros(count, np.int32), np.zeros(count, np.uint8), L)
+
+
+def _scalars(ol, oe, os_, bits, L):
+    out = []
+    for e in range(oe.shape[0]):
+        m = Matrix(1, 1, PrecisionContext(bits), ol[:, e:e + 1].copy(), oe[e:e + 1].copy(), os_[e:e + 1].copy())
+        out.append(m)
+    return out
+
+
+def max_rel_error(approx, ref) -> RelErrorStats:
+    """matrix.hpp:260-279 on the device: rel_error = RN(|RN(approx - ref)| / |ref|) at
+    ref's precision (precision.hpp:187-193); zero references skipped and counted."""
+    if approx.rows() != ref.rows() or approx.cols() != ref.cols():
+        raise DimensionError(f"shape mismatch: {approx.rows()}x{approx.cols()} vs {ref.rows()}x{ref.cols()}")
+    da, fa = _dev(approx)
+    dr, fr = _dev(ref)
+    ol, oe, os_, L = _metric_out(ref.bits(), 2)
+    skipped = C.c_int64(0)
+    try:
+        _raise(dr._h, _L.lib.mpgpu_max_rel_error(dr._h, C.byref(da.m), C.byref(dr.m), _ptr(ol), _ptr(oe),
+                                                 _ptr(os_), C.byref(skipped)))
+    finally:
+        if fa:
+            da.free()
+        if fr:
+            dr.free()
+    mx, mn = _scalars(ol, oe, os_, ref.bits(), L)
+    return RelErrorStats(mx, mn, int(skipped.value))
+
+
+def max_rel_error_solution(xhat, xtrue) -> SolutionError:
+    """blocklu.hpp:312-333 on the device (vectors as n x 1 matrices)."""
+    if xhat.rows() * xhat.cols() != xtrue.rows() * xtrue.cols():
+        raise DimensionError("solution error: length mismatch")
+    dx, fx = _dev(xhat)
+    dt, ft = _dev(xtrue)
+    ol, oe, os_, L = _metric_out(xtrue.bits(), 2)
+    zr = C.c_int64(0)
+    try:
+        _raise(dt._h, _L.lib.mpgpu_solution_error(dt._h, C.byref(dx.m), C.byref(dt.m), _ptr(ol), _ptr(oe),
+                                                  _ptr(os_), C.byref(zr)))
+    finally:
+        if fx:
+            dx.free()
+        if ft:
+            dt.free()
+    mr, mz = _scalars(ol, oe, os_, xtrue.bits(), L)
+    return SolutionError(mr, mz, int(zr.value))
+
+
+def one_norm(a) -> Matrix:
+    """matrix.hpp:237-251 on the device: 1x1 Matrix at a's precision."""
+    da, fa = _dev(a)
+    ol, oe, os_, L = _metric_out(a.bits(), 1)
+    try:
+        _raise(da._h, _L.lib.mpgpu_one_norm(da._h, C.byref(da.m), _ptr(ol), _ptr(oe), _ptr(os_)))
+    finally:
+        if fa:
+            da.free()
+    return _scalars(ol, oe, os_, a.bits(), L)[0]

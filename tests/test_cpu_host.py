@@ -113,5 +113,6 @@ def test_pad_even_and_equal_values(P):
 
 
 def test_mpgpu_nlimbs(P):
-    assert [P.nlimbs_for(b) for b in (2, 32, 33, 64, 65, 128, 129, 256, 512, 1024, 1025)] == \
-        [1, 1, 2, 2, 4, 4, 8, 8, 16, 32, 0]
+    # 1025..2048 bits: 64 limbs, storage / accuracy metrics only (mpgpu.h MPGPU_MAX_STORE_PREC)
+    assert [P.nlimbs_for(b) for b in (1, 2, 32, 33, 64, 65, 128, 129, 256, 512, 1024, 1025, 2048, 2049)] == \
+        [0, 1, 1, 2, 2, 4, 4, 8, 8, 16, 32, 64, 64, 0]

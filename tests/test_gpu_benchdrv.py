@@ -157,3 +157,15 @@ def test_cli_matmul_and_lu(tmp_path):
     r = subprocess.run([env_py, "-m", "paper_1410_1599_b200.cli", "lu", "--alpha-sweep", "x"], cwd=ROOT,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 1
+
+
+def test_wide_matrices_are_storage_only():
+    ctx = P.PrecisionContext(2048)
+    a = P.gen_uniform_full(3, 3, 1, ctx)
+    d = a.to_device()
+    assert P.identical(d.download(), a)  # upload / download round trip at 64 limbs
+    d.free()
+    with pytest.raises(P.DomainError):
+        P.simple_mul(a, a, ctx)
+    with pytest.raises(P.DomainError):
+        P.add(a, a)

@@ -104,6 +104,21 @@ struct DevBuf {
   uint32_t* u32() const { return static_cast<uint32_t*>(p); }
 };
 
+// Grow the device's stream-ordered pool (release threshold: keep everything) to at
+// least `bytes` with one allocate/free pair, so later allocations of the call are
+// sub-allocations of reserved memory.
+int ensure_pool(mpgpu_handle* h, size_t bytes) {
+  cudaMemPool_t pool;
+  CUDA_TRY(h, cudaDeviceGetMemPool(&pool, h->device));
+  uint64_t reserved = 0;
+  CUDA_TRY(h, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  if (reserved >= bytes) return MPGPU_OK;
+  void* p = nullptr;
+  CUDA_TRY(h, cudaMallocAsync(&p, bytes, h->stream));
+  CUDA_TRY(h, cudaFreeAsync(p, h->stream));
+  return MPGPU_OK;
+}
+
 // CUDA-event phase timers that never block: stop() records the end event and
 // queues (start, end, destination); flush_timers() (called once per API call, at
 // its final synchronisation) resolves every queued duration.  No host/GPU
@@ -216,6 +231,29 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   const bool timing = stats != nullptr;
+  if (algo == MPGPU_STRASSEN || algo == MPGPU_WINOGRAD) {
+    // grow the stream-ordered pool to the call's peak scratch once, before any timer:
+    // otherwise the first large call maps pages between its phases
+    const std::vector<Level> pl = plan_levels(m, l, n, param);
+    const size_t rec = sizeof(uint32_t) * S;
+    size_t peak = 0, nodes = 1, prevA = 0, prevB = 0;
+    std::vector<size_t> prodsz(pl.size(), 0);
+    for (size_t lev = 0; lev + 1 < pl.size(); ++lev) {
+      nodes *= 7;
+      const size_t a = rec * nodes * pl[lev + 1].m * pl[lev + 1].l, b = rec * nodes * pl[lev + 1].l * pl[lev + 1].n;
+      peak = std::max(peak, prevA + prevB + a + b);
+      prevA = a;
+      prevB = b;
+      prodsz[lev + 1] = rec * nodes * pl[lev + 1].m * pl[lev + 1].n;
+    }
+    if (pl.size() > 1) {
+      peak = std::max(peak, prevA + prevB + prodsz.back());
+      for (size_t lev = pl.size() - 1; lev >= 2; --lev) peak = std::max(peak, prodsz[lev] + prodsz[lev - 1]);
+      peak += rec * (size_t)(m * l + l * n + m * n);  // dense copies / top buffer, if needed
+      int rc = ensure_pool(h, peak + peak / 8);
+      if (rc) return rc;
+    }
+  }
   Timer total(timing, st);
   int launches = 0;
   auto leaf = [&](const uint32_t* a, int64_t la, const uint32_t* b, int64_t lb, uint32_t* c, int64_t lc,

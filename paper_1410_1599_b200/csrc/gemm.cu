@@ -78,8 +78,11 @@ struct GemmCfg<32> {
   static constexpr int MINB = MPG_MINB_32, TM = 8, TN = 16, TK = 4, U = 1;
 };
 
-template <int L, int TM, int TN, int TK, int U>
+template <int L, int TM, int TN, int TK, int U, bool FOLD>
 __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(const GemmArgs g) {
+  // FOLD: Block k-tiles (kb < l) -- a second accumulator and the C = RN(C + P) folds;
+  // without them (Simple, Strassen / Winograd leaves, LU Schur) the result is P itself
+  // (RN(-0 + P) == P), so acc and the per-step tile check are compiled out.
   constexpr int S = rec_stride(L);
   constexpr int NT = TM * TN;
   constexpr int TNB = TN * U;  // CTA tile width
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 #pragma unroll 1
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
-        if (k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
+        if (FOLD && k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             mp_add<L>(acc[u], pacc[u], 0u, g.sh, acc[u]);
@@ -180,7 +183,11 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     const int j = j0 + tx + u * TN;
     if (j >= g.n) break;
     MP<L> res;
-    mp_add<L>(acc[u], pacc[u], 0u, g.sh, res);
+    if constexpr (FOLD) {
+      mp_add<L>(acc[u], pacc[u], 0u, g.sh, res);
+    } else {
+      res = pacc[u];
+    }
     uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
     if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
       MP<L> old;
@@ -200,10 +207,13 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
   constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
   constexpr int S = rec_stride(L);
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
-  auto kern = gemm_leaf_kernel<L, TM, TN, TK, U>;
+  auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gemm_leaf_kernel<L, TM, TN, TK, U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(gemm_leaf_kernel<L, TM, TN, TK, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     configured = true;
   }
   dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, g.batch);

@@ -25,8 +25,12 @@
 #define MPG_MINB_1 4
 #define MPG_MINB_2 4
 #define MPG_MINB_4 3
-#define MPG_MINB_16 1
+#ifndef MPG_MINB_16
+#define MPG_MINB_16 6  // 80 registers: 6 CTAs of 128 threads per SM (measured best, 512-bit cfg)
+#endif
+#ifndef MPG_MINB_32
 #define MPG_MINB_32 1
+#endif
 #ifndef MPG_LOAD
 #define MPG_LOAD load_rec_s
 #endif

@@ -29,7 +29,7 @@
 #define MPG_MINB_16 6  // 80 registers: 6 CTAs of 128 threads per SM (measured best, 512-bit cfg)
 #endif
 #ifndef MPG_MINB_32
-#define MPG_MINB_32 1
+#define MPG_MINB_32 3  // 166 registers: 3 CTAs of 128 threads per SM (measured best, 1024-bit cfg)
 #endif
 #ifndef MPG_LOAD
 #define MPG_LOAD load_rec_s

@@ -28,6 +28,12 @@
 #ifndef MPG_MINB_16
 #define MPG_MINB_16 6  // 80 registers: 6 CTAs of 128 threads per SM (measured best, 512-bit cfg)
 #endif
+#ifndef MPG_TM_32
+#define MPG_TM_32 8
+#endif
+#ifndef MPG_TK_32
+#define MPG_TK_32 2  // measured: 2 > 4 > 8 at 1024 bits
+#endif
 #ifndef MPG_MINB_32
 #define MPG_MINB_32 3  // 166 registers: 3 CTAs of 128 threads per SM (measured best, 1024-bit cfg)
 #endif
@@ -47,6 +53,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
+
+#ifndef MPG_TK_8
+#define MPG_TK_8 16
+#endif
 
 #ifndef MPG_U_8
 #define MPG_U_8 1
@@ -71,7 +81,7 @@ struct GemmCfg<4> {
 };
 template <>
 struct GemmCfg<8> {
-  static constexpr int MINB = MPG_MINB_8, TM = 16, TN = 16, TK = 16, U = MPG_U_8;
+  static constexpr int MINB = MPG_MINB_8, TM = 16, TN = 16, TK = MPG_TK_8, U = MPG_U_8;
 };
 template <>
 struct GemmCfg<16> {
@@ -79,7 +89,7 @@ struct GemmCfg<16> {
 };
 template <>
 struct GemmCfg<32> {
-  static constexpr int MINB = MPG_MINB_32, TM = 8, TN = 16, TK = 4, U = 1;
+  static constexpr int MINB = MPG_MINB_32, TM = MPG_TM_32, TN = 16, TK = MPG_TK_32, U = 1;
 };
 
 template <int L, int TM, int TN, int TK, int U, bool FOLD>

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <initializer_list>
 #include <mutex>
 #include <string>
@@ -1057,6 +1058,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
   const int sh = 32 * A->nlimbs - A->prec;
   int64_t* zp = reinterpret_cast<int64_t*>(h->d_err + 2);
   Timer total(stats != nullptr, h->stream);
+  std::deque<mpgpu_stats> panel_stats;
   int rc = dispatch_L(A->nlimbs, [&](auto Lc) -> int {
     constexpr int L = decltype(Lc)::value;
     constexpr int S = rec_stride(L);
@@ -1068,6 +1070,16 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
     const bool coop = cand.alloc(h, 3 * sizeof(uint64_t) * kMaxGrid) == cudaSuccess &&
                       cudaMemsetAsync(cand.p, 0, 3 * sizeof(uint64_t) * kMaxGrid, st) == cudaSuccess &&
                       std::getenv("MPGPU_LU_PER_COLUMN") == nullptr;
+    DevBuf cbuf;
+    mpg::PivotCands pc;
+    if (pivoting) {
+      const int64_t cap = (n + 7) / 8 + 1;
+      CUDA_TRY(h, cbuf.alloc(h, cap * (sizeof(uint64_t) + sizeof(int64_t) + sizeof(int))));
+      pc.key = static_cast<uint64_t*>(cbuf.p);
+      pc.idx = reinterpret_cast<int64_t*>(pc.key + cap);
+      pc.cnt = reinterpret_cast<int*>(pc.idx + cap);
+      pc.cap = cap;
+    }
     auto panel = [&](int64_t p, int64_t k) {
       // pivot-free panels: one cooperative launch (measured 58.7 vs ~70 ms at n=2048);
       // pivoting: per-column kernels are as fast as the 3-barrier cooperative variant
@@ -1076,10 +1088,12 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
                                                reinterpret_cast<int64_t*>(static_cast<uint64_t*>(cand.p) + kMaxGrid),
                                                kMaxGrid, st) == 0)
         return;
+      int64_t ncand = 0;  // candidates written by the previous step (0: scan the column)
       for (int64_t d = p; d < p + k; ++d) {
-        if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, st);
-        mpg::launch_lu_step<L>(a, n, d, n, p + k, sh, h->d_err, st);
+        if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, pc, ncand, p, p + k, st);
+        ncand = mpg::launch_lu_step<L>(a, n, d, n, p + k, sh, h->d_err, pivoting ? pc : mpg::PivotCands{}, st);
       }
+      if (pivoting) mpg::launch_laswp<L>(a, n, p, k, h->d_piv, zp, st);
     };
     while (n - off > K) {
       const int64_t rest = n - off - K;
@@ -1088,7 +1102,8 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       const uint32_t* l21 = a + ((off + K) * n + off) * S;
       const uint32_t* u12 = a + (off * n + off + K) * S;
       uint32_t* a22 = a + ((off + K) * n + off + K) * S;
-      mpgpu_stats ss{};
+      panel_stats.emplace_back();
+      mpgpu_stats& ss = panel_stats.back();  // deque: stable address until the final flush
       if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) {
         int r = run_gemm<L>(h, kernel, n_min, l21, n, u12, n, a22, n, rest, K, rest, sh, stats ? &ss : nullptr, 1);
         if (r) return r;
@@ -1105,17 +1120,21 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
         count_fast_rec(kernel, rest, K, rest, n_min, c);
         stats->mul += c[0];
         stats->addsub += c[1];
-        flush_timers();  // ss is local: resolve its queued timings now
-        stats->leaf_ms += ss.leaf_ms;
-        stats->leaf_madds += ss.leaf_madds;
-        stats->launches += ss.launches;
       }
       off += K;
     }
     panel(off, n - off);
     return 0;
   });
-  if (stats) total.stop(&stats->device_ms);
+  if (stats) {
+    total.stop(&stats->device_ms);
+    flush_timers();  // resolve the Schur GEMMs' queued timings (no host sync per panel)
+    for (const mpgpu_stats& ss : panel_stats) {
+      stats->leaf_ms += ss.leaf_ms;
+      stats->leaf_madds += ss.leaf_madds;
+      stats->launches += ss.launches;
+    }
+  }
   if (rc) return rc;
   int64_t zpv = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&zpv, zp, sizeof zpv, cudaMemcpyDeviceToHost, h->stream));

@@ -71,17 +71,32 @@ void launch_vec_op(int op, const uint32_t* A, const uint32_t* B, uint32_t* C, in
                    uint32_t* err, cudaStream_t st);
 
 // ---- LU (blocklu.hpp:42-146) --------------------------------------------
+// Pivot-search candidates: one (compact magnitude key, first row, multiplicity) per
+// lu_col CTA for the next column (cap entries each).
+struct PivotCands {
+  uint64_t* key = nullptr;
+  int64_t* idx = nullptr;
+  int* cnt = nullptr;
+  int64_t cap = 0;
+};
 // One right-looking elimination step d of the panel [p, row_end) x [p, p+k) of the
 // n x n record matrix a (row-major, ld = n):
 //   multipliers a_id = RN(a_id / a_dd) for i in (d, row_end), and
 //   a_ij = RN(a_ij - RN(a_id * a_dj)) for i in (d, row_end), j in (d, p+k).
+// With cand.key set, also writes the pivot candidates of column d+1; returns their
+// count (0: none written).
 template <int L>
-void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh,
-                    uint32_t* err, cudaStream_t st);
-// pivot search for column d over rows [d, row_end): first max |a_id| -> piv_dev[d];
-// then swap rows d and piv over all n columns.
+int64_t launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh, uint32_t* err,
+                       const PivotCands& cand, cudaStream_t st);
+// pivot search for column d over rows [d, row_end): first max |a_id| -> piv_dev[d],
+// from ncand candidates of the previous step (ncand > 0) or a column scan; then swap
+// rows d and piv over the columns [c0, c1).
 template <int L>
 void launch_pivot(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t* piv_dev, int64_t* zp,
+                  const PivotCands& cand, int64_t ncand, int64_t c0, int64_t c1, cudaStream_t st);
+// apply the panel's interchanges piv[p .. p+k) to all columns outside [p, p+k)
+template <int L>
+void launch_laswp(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv_dev, const int64_t* zp,
                   cudaStream_t st);
 // forward substitution step s of trsm_unit_lower (blocklu.hpp:60-69) on the
 // block rows (s, p_end) x cols [c0, c0+w): a_ij = RN(a_ij - RN(a_is * a_sj)).

@@ -35,9 +35,27 @@ inline int blocks_for(int64_t n) {
 // Every row's multiplier is produced inside the CTA that uses it, so one launch
 // per column suffices (no grid-wide dependency between rows).
 constexpr int LU_RB = 8;
+__device__ __forceinline__ uint64_t mag_key(uint32_t e, uint32_t top) {
+  return e == (uint32_t)EXP_ZERO ? 0ull : (((uint64_t)(e ^ 0x80000000u)) << 32) | top;
+}
+// (key, first index, count) of the rows whose compact magnitude key is maximal;
+// count 0 marks an empty candidate
+__device__ __forceinline__ void piv_combine(uint64_t& k, int64_t& i, int& c, uint64_t k2, int64_t i2, int c2) {
+  if (c2 == 0) return;
+  if (c == 0 || k2 > k) {
+    k = k2;
+    i = i2;
+    c = c2;
+  } else if (k2 == k) {
+    i = i2 < i ? i2 : i;
+    c += c2;
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(NT) lu_col_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end,
-                                                    int64_t col_end, int sh, int64_t* zp) {
+                                                    int64_t col_end, int sh, int64_t* zp, uint64_t* ck,
+                                                    int64_t* ci, int* cc) {
   constexpr int S = rec_stride(L);
   __shared__ __align__(16) uint32_t s_mult[LU_RB * S];
   if (*zp) return;  // a zero pivot was already met: the factorisation has failed
@@ -71,6 +89,35 @@ __global__ void __launch_bounds__(NT) lu_col_kernel(uint32_t* a, int64_t n, int6
     mp_add<L>(x, p, 1u, sh, x);
     store_rec<L>(a + (i * n + j) * S, x);
   }
+  if (ck != nullptr && d + 1 < col_end) {
+    // pivot candidates of column d+1 over this CTA's rows (it just updated them), so
+    // the next pivot search reduces one record per CTA instead of scanning the column
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int64_t i = r0 + threadIdx.x;
+      uint64_t k = 0;
+      int64_t idx = INT64_MAX;
+      int c = 0;
+      if (threadIdx.x < LU_RB && i < row_end) {
+        const uint32_t* r = a + (i * n + d + 1) * S;
+        k = mag_key(r[L], r[L - 1]);
+        idx = i;
+        c = 1;
+      }
+#pragma unroll
+      for (int o = LU_RB / 2; o > 0; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, k, o);
+        const int64_t i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, c, o);
+        piv_combine(k, idx, c, k2, i2, c2);
+      }
+      if (threadIdx.x == 0) {
+        ck[blockIdx.x] = k;
+        ci[blockIdx.x] = idx;
+        cc[blockIdx.x] = c;
+      }
+    }
+  }
 }
 
 // trsm_unit_lower step s: rows (s, p_end), cols [c0, c0 + w)
@@ -91,78 +138,73 @@ __global__ void trsm_l_kernel(uint32_t* a, int64_t n, int64_t s, int64_t p_end, 
   }
 }
 
-// pivot search (first maximal |a_id| over rows [d, row_end)) + full-row swap.
-// Phase 1 reduces a 64-bit magnitude key (biased exponent : top limb) with warp
-// shuffles; rows whose key ties with the maximum are then resolved by a full MP
-// comparison (first maximal row wins), which only runs when a tie exists.
+// pivot search (first maximal |a_id| over rows [d, row_end)) + swap of rows d and the
+// pivot over the panel columns [c0, c1) (the other columns are swapped once per panel by
+// laswp_kernel -- row swaps commute with work on columns they do not touch).  The
+// compact magnitude key (biased exponent : top limb) is reduced with its first index
+// and its multiplicity, from the previous step's per-CTA candidates when given
+// (ncand > 0) or by scanning the column; only when several rows share the maximal key
+// does a full MP comparison (first maximal row wins) run.
 constexpr int PIV_NT = 1024;
-__device__ __forceinline__ uint64_t mag_key(uint32_t e, uint32_t top) {
-  return e == (uint32_t)EXP_ZERO ? 0ull : (((uint64_t)(e ^ 0x80000000u)) << 32) | top;
-}
 template <int L>
 __global__ void __launch_bounds__(PIV_NT) pivot_kernel(uint32_t* a, int64_t n, int64_t d, int64_t row_end,
-                                                       int64_t* piv, int64_t* zp) {
+                                                       int64_t* piv, int64_t* zp, const uint64_t* ck,
+                                                       const int64_t* ci, const int* cc, int64_t ncand, int64_t c0,
+                                                       int64_t c1) {
   constexpr int S = rec_stride(L);
   __shared__ uint64_t s_key[PIV_NT / 32];
   __shared__ int64_t s_idx[PIV_NT / 32];
-  __shared__ uint64_t s_best_key;
+  __shared__ int s_cnt[PIV_NT / 32];
   __shared__ int64_t s_best;
   __shared__ int s_ties;
+  __shared__ uint64_t s_kstar;
   if (*zp) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint64_t bk = 0;
   int64_t bi = INT64_MAX;
-  for (int64_t i = d + tid; i < row_end; i += PIV_NT) {
-    const uint32_t* r = a + (i * n + d) * S;
-    const uint64_t k = mag_key(r[L], r[L - 1]);
-    if (bi == INT64_MAX || k > bk) {
-      bk = k;
-      bi = i;
+  int bc = 0;
+  if (ncand > 0) {
+    // written by the previous step's CTAs over rows [d, row_end) of column d
+    for (int64_t t = tid; t < ncand; t += PIV_NT) piv_combine(bk, bi, bc, ck[t], ci[t], cc[t]);
+  } else {
+    for (int64_t i = d + tid; i < row_end; i += PIV_NT) {
+      const uint32_t* r = a + (i * n + d) * S;
+      piv_combine(bk, bi, bc, mag_key(r[L], r[L - 1]), i, 1);
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
     const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (k2 > bk || (k2 == bk && i2 < bi)) {
-      bk = k2;
-      bi = i2;
-    }
+    const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+    piv_combine(bk, bi, bc, k2, i2, c2);
   }
   if (lane == 0) {
     s_key[wid] = bk;
     s_idx[wid] = bi;
+    s_cnt[wid] = bc;
   }
-  if (tid == 0) s_ties = 0;
   __syncthreads();
   if (wid == 0) {
     bk = s_key[lane];
     bi = s_idx[lane];
+    bc = s_cnt[lane];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
       const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (k2 > bk || (k2 == bk && i2 < bi)) {
-        bk = k2;
-        bi = i2;
-      }
+      const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+      piv_combine(bk, bi, bc, k2, i2, c2);
     }
     if (lane == 0) {
-      s_best_key = bk;
       s_best = bi;
+      s_ties = bc;
+      s_kstar = bk;
     }
   }
   __syncthreads();
-  // ties on the compact key: count them
-  const uint64_t kstar = s_best_key;
-  int mine = 0;
-  for (int64_t i = d + tid; i < row_end; i += PIV_NT) {
-    const uint32_t* r = a + (i * n + d) * S;
-    mine += mag_key(r[L], r[L - 1]) == kstar;
-  }
-  if (mine) atomicAdd(&s_ties, mine);
-  __syncthreads();
   if (s_ties > 1 && tid == 0) {  // rare: full comparison among the tied rows
+    const uint64_t kstar = s_kstar;
     int64_t r = -1;
     MP<L> rv;
     mp_zero(rv);
@@ -183,13 +225,35 @@ __global__ void __launch_bounds__(PIV_NT) pivot_kernel(uint32_t* a, int64_t n, i
   if (tid == 0) piv[d] = r;
   if (r != d) {
     constexpr int CH = S / 4;
-    for (int64_t t = tid; t < n * CH; t += PIV_NT) {
-      const int64_t j = t / CH, w = t % CH;
+    for (int64_t t = tid; t < (c1 - c0) * CH; t += PIV_NT) {
+      const int64_t j = c0 + t / CH, w = t % CH;
       uint4* p = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
       uint4* q = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
       const uint4 tmp = *p;
       *p = *q;
       *q = tmp;
+    }
+  }
+}
+
+// the panel's row interchanges d = p .. p+k-1 (in order) on every column outside
+// [p, p+k) -- LAPACK laswp; each 16-byte chunk of a column is independent
+template <int L>
+__global__ void laswp_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv, const int64_t* zp) {
+  constexpr int S = rec_stride(L), CH = S / 4;
+  if (*zp) return;
+  const int64_t total = (n - k) * CH;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = t / CH, w = t - jj * CH;
+    const int64_t j = jj < p ? jj : jj + k;
+    for (int64_t d = p; d < p + k; ++d) {
+      const int64_t r = piv[d];
+      if (r == d) continue;
+      uint4* x = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
+      uint4* y = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
+      const uint4 tmp = *x;
+      *x = *y;
+      *y = tmp;
     }
   }
 }
@@ -558,19 +622,29 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
 }
 
 template <int L>
-void launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh, uint32_t* err,
-                    cudaStream_t st) {
+int64_t launch_lu_step(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t col_end, int sh, uint32_t* err,
+                       const PivotCands& cand, cudaStream_t st) {
   // zero-pivot flag lives right after the error word (see capi.cu)
   int64_t* zp = reinterpret_cast<int64_t*>(err + 2);
   const int64_t rows = row_end - d - 1;
   const int blocks = (int)((rows + LU_RB - 1) / LU_RB);
-  lu_col_kernel<L><<<blocks < 1 ? 1 : blocks, NT, 0, st>>>(a, n, d, row_end, col_end, sh, zp);
+  const bool want = cand.key != nullptr && d + 1 < col_end && rows > 0 && blocks <= cand.cap;
+  lu_col_kernel<L><<<blocks < 1 ? 1 : blocks, NT, 0, st>>>(a, n, d, row_end, col_end, sh, zp,
+                                                           want ? cand.key : nullptr, cand.idx, cand.cnt);
+  return want ? blocks : 0;
 }
 
 template <int L>
 void launch_pivot(uint32_t* a, int64_t n, int64_t d, int64_t row_end, int64_t* piv_dev, int64_t* zp,
+                  const PivotCands& cand, int64_t ncand, int64_t c0, int64_t c1, cudaStream_t st) {
+  pivot_kernel<L><<<1, PIV_NT, 0, st>>>(a, n, d, row_end, piv_dev, zp, cand.key, cand.idx, cand.cnt, ncand, c0, c1);
+}
+
+template <int L>
+void launch_laswp(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv_dev, const int64_t* zp,
                   cudaStream_t st) {
-  pivot_kernel<L><<<1, PIV_NT, 0, st>>>(a, n, d, row_end, piv_dev, zp);
+  if (n - k <= 0) return;
+  laswp_kernel<L><<<blocks_for((n - k) * (rec_stride(L) / 4)), NT, 0, st>>>(a, n, p, k, piv_dev, zp);
 }
 
 template <int L>
@@ -596,8 +670,11 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
 }
 
 #define MPG_LU_INST(L)                                                                                      \
-  template void launch_lu_step<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int, uint32_t*, cudaStream_t); \
-  template void launch_pivot<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t*, int64_t*, cudaStream_t);        \
+  template int64_t launch_lu_step<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int, uint32_t*,              \
+                                     const PivotCands&, cudaStream_t);                                           \
+  template void launch_pivot<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t*, int64_t*, const PivotCands&,    \
+                                int64_t, int64_t, int64_t, cudaStream_t);                                       \
+  template void launch_laswp<L>(uint32_t*, int64_t, int64_t, int64_t, const int64_t*, const int64_t*, cudaStream_t); \
   template void launch_trsm_l_step<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int, uint32_t*,   \
                                       cudaStream_t);                                                            \
   template void launch_trsm_l_panel<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t); \

@@ -1070,6 +1070,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
     const bool coop = cand.alloc(h, 3 * sizeof(uint64_t) * kMaxGrid) == cudaSuccess &&
                       cudaMemsetAsync(cand.p, 0, 3 * sizeof(uint64_t) * kMaxGrid, st) == cudaSuccess &&
                       std::getenv("MPGPU_LU_PER_COLUMN") == nullptr;
+    const bool coop_piv = std::getenv("MPGPU_LU_PIVOT_PER_COLUMN") == nullptr;
     DevBuf cbuf;
     mpg::PivotCands pc;
     if (pivoting) {
@@ -1081,13 +1082,15 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       pc.cap = cap;
     }
     auto panel = [&](int64_t p, int64_t k) {
-      // pivot-free panels: one cooperative launch (measured 58.7 vs ~70 ms at n=2048);
-      // pivoting: per-column kernels are as fast as the 3-barrier cooperative variant
-      if (coop && !pivoting && mpg::launch_lu_panel_coop<L>(a, n, p, k, n, pivoting, h->d_piv, zp, sh,
-                                               static_cast<uint64_t*>(cand.p),
-                                               reinterpret_cast<int64_t*>(static_cast<uint64_t*>(cand.p) + kMaxGrid),
-                                               kMaxGrid, st) == 0)
+      // one cooperative launch per panel (grid barriers instead of kernel boundaries:
+      // 1 per column pivot-free, 2 with pivoting); per-column kernels otherwise
+      if (coop && (!pivoting || coop_piv) &&
+          mpg::launch_lu_panel_coop<L>(a, n, p, k, n, pivoting, h->d_piv, zp, sh, static_cast<uint64_t*>(cand.p),
+                                       reinterpret_cast<int64_t*>(static_cast<uint64_t*>(cand.p) + kMaxGrid),
+                                       kMaxGrid, st) == 0) {
+        if (pivoting) mpg::launch_laswp<L>(a, n, p, k, h->d_piv, zp, st);
         return;
+      }
       int64_t ncand = 0;  // candidates written by the previous step (0: scan the column)
       for (int64_t d = p; d < p + k; ++d) {
         if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, pc, ncand, p, p + k, st);

@@ -414,151 +414,110 @@ __global__ void __launch_bounds__(NT) lu_panel_coop_kernel(uint32_t* a, int64_t 
   extern __shared__ __align__(16) uint32_t s_mult[];
   __shared__ uint64_t s_wk[NT / 32];
   __shared__ int64_t s_wi[NT / 32];
+  __shared__ int s_wc[NT / 32];
   __shared__ int64_t s_piv;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rows_all = row_end - p;
   const int64_t chunk = (rows_all + gridDim.x - 1) / gridDim.x;
   const int64_t lo = p + (int64_t)blockIdx.x * chunk;
   const int64_t hi = min(row_end, lo + chunk);
+  // pivot candidates of column d over this CTA's rows [max(d, lo), hi): (compact key,
+  // first row, multiplicity), block-reduced, one record per CTA
+  auto candidates = [&](int64_t col, int64_t from) {
+    uint64_t bk = 0;
+    int64_t bi = INT64_MAX;
+    int bc = 0;
+    for (int64_t i = max(from, lo) + tid; i < hi; i += NT) {
+      const uint32_t* r = a + (i * n + col) * S;
+      piv_combine(bk, bi, bc, mag_key(r[L], r[L - 1]), i, 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+      piv_combine(bk, bi, bc, k2, i2, c2);
+    }
+    if (lane == 0) {
+      s_wk[wid] = bk;
+      s_wi[wid] = bi;
+      s_wc[wid] = bc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < NT / 32; ++w) piv_combine(bk, bi, bc, s_wk[w], s_wi[w], s_wc[w]);
+      cand_key[blockIdx.x] = bk;
+      cand_idx[blockIdx.x] = bi;
+      cand_cnt[blockIdx.x] = (uint64_t)bc;
+    }
+    __syncthreads();
+  };
+  if (pivoting) {
+    candidates(p, p);
+    grid.sync();
+  }
   for (int64_t d = p; d < p + k; ++d) {
     if (pivoting) {
-      // (1) CTA-local best (key, idx) over rows [max(d, lo), hi) and how many of
-      //     the CTA's rows share that key
-      uint64_t bk = 0;
-      int64_t bi = INT64_MAX;
-      for (int64_t i = max(d, lo) + tid; i < hi; i += NT) {
-        const uint32_t* r = a + (i * n + d) * S;
-        const uint64_t kk = mag_key(r[L], r[L - 1]);
-        if (bi == INT64_MAX || kk > bk) {
-          bk = kk;
-          bi = i;
-        }
-      }
-      auto better = [](uint64_t k1, int64_t i1, uint64_t k0, int64_t i0) {
-        return i1 != INT64_MAX && (i0 == INT64_MAX || k1 > k0 || (k1 == k0 && i1 < i0));
-      };
+      // every CTA reduces the same candidate list -> the same pivot
+      uint64_t gk = 0;
+      int64_t gi = INT64_MAX;
+      int gc = 0;
+      for (unsigned b = tid; b < gridDim.x; b += NT) piv_combine(gk, gi, gc, cand_key[b], cand_idx[b], (int)cand_cnt[b]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(k2, i2, bk, bi)) {
-          bk = k2;
-          bi = i2;
-        }
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, gk, o);
+        const int64_t i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int c2 = __shfl_xor_sync(0xffffffffu, gc, o);
+        piv_combine(gk, gi, gc, k2, i2, c2);
       }
       if (lane == 0) {
-        s_wk[wid] = bk;
-        s_wi[wid] = bi;
+        s_wk[wid] = gk;
+        s_wi[wid] = gi;
+        s_wc[wid] = gc;
       }
       __syncthreads();
-      if (wid == 0) {
-        bk = lane < NT / 32 ? s_wk[lane] : 0;
-        bi = lane < NT / 32 ? s_wi[lane] : INT64_MAX;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-          const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (better(k2, i2, bk, bi)) {
-            bk = k2;
-            bi = i2;
-          }
-        }
-        if (lane == 0) {
-          s_wk[0] = bk;
-          s_wi[0] = bi;
-        }
-      }
-      __syncthreads();
-      {
-        const uint64_t kb = s_wk[0];
-        int cnt = 0;
-        for (int64_t i = max(d, lo) + tid; i < hi; i += NT) {
-          const uint32_t* r = a + (i * n + d) * S;
-          cnt += mag_key(r[L], r[L - 1]) == kb;
-        }
-        cnt = __syncthreads_count(cnt > 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0;
-        if (lane == 0 && s_wi[0] != INT64_MAX) atomicAdd(reinterpret_cast<unsigned long long*>(&cand_cnt[blockIdx.x]), (unsigned long long)cnt);
-      }
       if (tid == 0) {
-        cand_key[blockIdx.x] = s_wk[0];
-        cand_idx[blockIdx.x] = s_wi[0];
-      }
-      grid.sync();
-      // (2) every CTA reduces the same candidate list -> the same pivot
-      {
-        uint64_t gk = 0;
-        int64_t gi = INT64_MAX;
-        for (unsigned b = tid; b < gridDim.x; b += NT) {
-          if (better(cand_key[b], cand_idx[b], gk, gi)) {
-            gk = cand_key[b];
-            gi = cand_idx[b];
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, gk, o);
-          const int64_t i2 = __shfl_xor_sync(0xffffffffu, gi, o);
-          if (better(k2, i2, gk, gi)) {
-            gk = k2;
-            gi = i2;
-          }
-        }
-        __syncthreads();
-        if (lane == 0) {
-          s_wk[wid] = gk;
-          s_wi[wid] = gi;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          for (int w = 1; w < NT / 32; ++w)
-            if (better(s_wk[w], s_wi[w], gk, gi)) {
-              gk = s_wk[w];
-              gi = s_wi[w];
+        for (int w = 1; w < NT / 32; ++w) piv_combine(gk, gi, gc, s_wk[w], s_wi[w], s_wc[w]);
+        if (gc > 1) {  // rows sharing the winning compact key: a full comparison decides (rare)
+          MP<L> rv, x;
+          int64_t r = -1;
+          for (int64_t i = d; i < row_end; ++i) {
+            const uint32_t* q = a + (i * n + d) * S;
+            if (mag_key(q[L], q[L - 1]) != gk) continue;
+            load_rec<L>(q, x);
+            if (r < 0 || mp_cmpabs<L>(x, rv) > 0) {
+              rv = x;
+              r = i;
             }
-          // rows sharing the winning compact key: a full comparison decides (rare)
-          unsigned long long ties = 0;
-          for (unsigned b = 0; b < gridDim.x; ++b)
-            if (cand_idx[b] != INT64_MAX && cand_key[b] == gk) ties += cand_cnt[b];
-          if (ties > 1) {
-            MP<L> rv, x;
-            int64_t r = -1;
-            for (int64_t i = d; i < row_end; ++i) {
-              const uint32_t* q = a + (i * n + d) * S;
-              if (mag_key(q[L], q[L - 1]) != gk) continue;
-              load_rec<L>(q, x);
-              if (r < 0 || mp_cmpabs<L>(x, rv) > 0) {
-                rv = x;
-                r = i;
-              }
-            }
-            gi = r;
           }
-          s_piv = gi;
-          if (blockIdx.x == 0) piv[d] = gi;
+          gi = r;
         }
+        s_piv = gi;
       }
       __syncthreads();
       const int64_t r = s_piv;
-      if (r != d) {  // (3) swap rows d, r: columns split over CTAs
-        constexpr int CH = S / 4;
-        for (int64_t t = (int64_t)blockIdx.x * NT + tid; t < n * CH; t += (int64_t)gridDim.x * NT) {
-          const int64_t j = t / CH, w = t % CH;
-          uint4* pp = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
-          uint4* qq = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
-          const uint4 tmp = *pp;
-          *pp = *qq;
-          *qq = tmp;
+      if (blockIdx.x == 0) {
+        if (tid == 0) piv[d] = r;
+        if (r != d) {  // swap rows d, r over the panel columns (laswp does the rest)
+          constexpr int CH = S / 4;
+          for (int64_t t = tid; t < k * CH; t += NT) {
+            const int64_t j = p + t / CH, w = t % CH;
+            uint4* pp = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
+            uint4* qq = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
+            const uint4 tmp = *pp;
+            *pp = *qq;
+            *qq = tmp;
+          }
         }
       }
       grid.sync();
     }
-    if (pivoting && tid == 0) cand_cnt[blockIdx.x] = 0;  // read by all CTAs before the swap sync
-    // (4) zero pivot: every CTA sees the same a_dd and stops (blocklu.hpp:46-47)
+    // zero pivot: every CTA sees the same a_dd and stops (blocklu.hpp:46-47)
     if (a[(d * n + d) * S + L] == (uint32_t)EXP_ZERO) {
       if (blockIdx.x == 0 && tid == 0) *zp = d + 1;
       return;
     }
-    // (5) multipliers and rank-1 update for this CTA's rows in (d, row_end)
+    // multipliers and rank-1 update for this CTA's rows in (d, row_end)
     const int64_t r0 = max(d + 1, lo);
     const int64_t nr = hi - r0;
     if (nr > 0) {
@@ -582,6 +541,10 @@ __global__ void __launch_bounds__(NT) lu_panel_coop_kernel(uint32_t* a, int64_t 
         mp_add<L>(x, pr, 1u, sh, x);
         store_rec<L>(a + ((r0 + rr) * n + j) * S, x);
       }
+    }
+    if (pivoting && d + 1 < p + k) {
+      __syncthreads();  // this CTA's updates of column d+1 are visible to its threads
+      candidates(d + 1, d + 1);
     }
     grid.sync();
   }

@@ -399,3 +399,48 @@ def run_lu(kind, n, bits, kernel, n_min, alpha_lo, alpha_hi, seed=1, verbose=Fal
                             C.c_int64(n_min), C.c_int64(alpha_lo), C.c_int64(alpha_hi), C.c_uint64(seed),
                             int(verbose), buf, C.c_int64(len(buf)), C.byref(s)))
     return buf.value.decode(), bool(s.value)
+
+
+# ---- text codec / op-count tables (compiled reference) ----------------------
+
+def from_hex(text, bits):
+    """-> (OMat 1x1, None) or (None, parse error position)"""
+    x = OMat(1, 1, bits)
+    pos = C.c_int64(-1)
+    rc = ref().ref_from_hex(text.encode(), C.c_long(bits), x.nlimbs, *_soa(x), C.byref(pos))
+    if rc == 7:
+        return None, int(pos.value)
+    _check(rc)
+    return x, None
+
+
+def write_matrix(x):
+    n = x.rows() * x.cols()
+    buf = C.create_string_buffer(n * (x.bits() // 4 + 32) + 64)
+    _check(ref().ref_write_matrix(C.c_long(x.bits()), x.nlimbs, C.c_int64(x.rows()), C.c_int64(x.cols()), *_soa(x),
+                                  buf, C.c_int64(len(buf))))
+    return buf.value.decode()
+
+
+def read_matrix(text, cap=1 << 16, max_bits=4096):
+    """-> OMat, or raises OracleError (rc 1 DimensionError, 4 IoError, ...)"""
+    L = (max_bits + 31) // 32
+    lim = np.zeros((L, cap), np.uint32)
+    ex = np.zeros(cap, np.int32)
+    sg = np.zeros(cap, np.uint8)
+    dims = (C.c_int64 * 3)()
+    _check(ref().ref_read_matrix(text.encode(), L, C.c_int64(cap), dims, _p(lim), _p(ex), _p(sg)))
+    m, n, bits = (int(v) for v in dims)
+    N = m * n
+    Lb = (bits + 31) // 32
+    # stored as L planes of stride N (most significant plane L-1): keep the top Lb planes
+    planes = lim.reshape(-1)[:L * N].reshape(L, N)
+    return OMat(m, n, bits, planes[L - Lb:].copy(), ex[:N].copy(), sg[:N].copy())
+
+
+def ratio_table(sizes, n_min, fmt="table"):
+    arr = (C.c_int64 * len(sizes))(*sizes)
+    buf = C.create_string_buffer(1 << 16)
+    _check(ref().ref_ratio_table(0 if fmt == "table" else 1, arr, len(sizes), C.c_int64(n_min), buf,
+                                 C.c_int64(len(buf))))
+    return buf.value.decode()

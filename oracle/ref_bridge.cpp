@@ -481,4 +481,63 @@ int ref_run_lu(int kind, std::int64_t n, long bits, int kernel, std::int64_t n_m
   });
 }
 
+// ---- text codec and op-count tables (precision.hpp:204-300, matrix.hpp:309-344,
+// opmodel.hpp:46-155) -- checkers of the host codec and the CLI's opcount ----
+int ref_from_hex(const char* text, long prec, int L, std::uint32_t* xl, std::int32_t* xe, std::uint8_t* xs,
+                 std::int64_t* err_pos) {
+  try {
+    Matrix m(1, 1, PrecisionContext(prec));
+    m.at(0, 0) = from_hex(text, PrecisionContext(prec));
+    return store(m, L, xl, xe, xs);
+  } catch (const ParseError& e) {
+    *err_pos = static_cast<std::int64_t>(e.position);
+    return 7;
+  } catch (...) {
+    return 5;
+  }
+}
+
+int ref_write_matrix(long prec, int L, std::int64_t rows, std::int64_t cols, const std::uint32_t* xl,
+                     const std::int32_t* xe, const std::uint8_t* xs, char* buf, std::int64_t buflen) {
+  return guarded([&] {
+    Matrix m = load(rows, cols, prec, L, xl, xe, xs);
+    std::ostringstream os;
+    write_matrix(os, m);
+    const std::string t = os.str();
+    if (static_cast<std::int64_t>(t.size()) + 1 > buflen) return 1;
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+  });
+}
+
+// read_matrix: dims[3] = {m, n, bits}; the SoA buffers hold cap elements of L limbs
+int ref_read_matrix(const char* text, int L, std::int64_t cap, std::int64_t* dims, std::uint32_t* xl,
+                    std::int32_t* xe, std::uint8_t* xs) {
+  return guarded([&] {
+    std::istringstream is(text);
+    Matrix m = read_matrix(is);
+    dims[0] = static_cast<std::int64_t>(m.rows());
+    dims[1] = static_cast<std::int64_t>(m.cols());
+    dims[2] = m.bits();
+    if (static_cast<std::int64_t>(m.rows() * m.cols()) > cap || (m.bits() + 31) / 32 > L) return 1;
+    return store(m, L, xl, xe, xs);
+  });
+}
+
+// opcount table (format 0: text, 1: csv) over n x n x n sizes
+int ref_ratio_table(int format, const std::int64_t* sizes, int count, std::int64_t n_min, char* buf,
+                    std::int64_t buflen) {
+  return guarded([&] {
+    std::vector<Dims3> dims;
+    for (int i = 0; i < count; ++i)
+      dims.push_back(Dims3{static_cast<std::size_t>(sizes[i]), static_cast<std::size_t>(sizes[i]),
+                           static_cast<std::size_t>(sizes[i])});
+    const auto rows = ratio_table(dims, static_cast<std::size_t>(n_min));
+    const std::string t = format == 0 ? format_ratio_table(rows) : format_ratio_csv(rows);
+    if (static_cast<std::int64_t>(t.size()) + 1 > buflen) return 1;
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+  });
+}
+
 }  // extern "C"

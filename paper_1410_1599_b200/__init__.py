@@ -10,7 +10,9 @@ from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix
                    solve_columnwise, sub, vec_op, UndefinedMetricError, RelErrorStats, SolutionError,
                    max_rel_error, max_rel_error_solution, one_norm)
 from .matgen import Prng64, from_ints, gen_random, gen_scaled, gen_uniform_full, to_fractions
+from .codec import IoError, ParseError, from_hex, read_matrix, to_hex, write_matrix
 from .benchdrv import (CSV_HEADER, BenchRecord, LUOutcome, LURequest, MatmulRequest, append_csv, bench_reference,
-                       gen_bench_pair, gen_linear_system, gen_lotkin, print_csv, run_lu, run_matmul)
+                       gen_bench_pair, gen_linear_system, gen_lotkin, print_csv, run_lu, run_matmul, ratio_table,
+                       format_ratio_csv, format_ratio_table)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

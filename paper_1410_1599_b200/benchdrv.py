@@ -277,3 +277,85 @@ def run_lu(q: LURequest) -> LUOutcome:
             out.any_singular = True
         out.rows.append(rec)
     return out
+
+
+# ---------------------------------------------------------------------------
+# analytic operation-count ratios (opmodel.hpp:46-155; CLI `opcount`)
+# ---------------------------------------------------------------------------
+
+
+def _fixed3(num: int, den: int) -> str:
+    """Ratio::fixed3 (opmodel.hpp:59-67): 3 fractional digits, half away from zero."""
+    q = (num * 2000 + den) // (den * 2)
+    return f"{q // 1000}.{q % 1000:03d}"
+
+
+def ratio_table(sizes, n_min: int):
+    """opmodel.hpp:81-106: per size (m, l, n) the Strassen / Winograd mul and addsub
+    counts relative to Simple, as reduced fractions."""
+    from math import gcd
+    from .mpmm import DimensionError, count_fast
+    if not sizes:
+        raise DimensionError("ratio_table: empty size list")
+    rows = []
+    for (m, l, n) in sizes:
+        s = count_simple(m, l, n)
+        st = count_fast(Algorithm.strassen, m, l, n, n_min)
+        wi = count_fast(Algorithm.winograd, m, l, n, n_min)
+
+        def ratio(a, b):
+            if b == 0:
+                if a == 0:
+                    return (1, 1)
+                raise DomainError("addsub ratio undefined: simple algorithm performs no additions")
+            g = gcd(a, b)
+            return (a // g, b // g)
+        rows.append(((m, l, n), n_min, ratio(st.mul, s.mul), ratio(st.addsub, s.addsub), ratio(wi.mul, s.mul),
+                     ratio(wi.addsub, s.addsub)))
+    return rows
+
+
+def format_ratio_csv(rows) -> str:
+    """opmodel.hpp:143-155"""
+    out = ["m,l,n,n_min,strassen_mul_ratio,strassen_addsub_ratio,winograd_mul_ratio,winograd_addsub_ratio"]
+    for (m, l, n), nm, sm, sa, wm, wa in rows:
+        out.append(f"{m},{l},{n},{nm},{_fixed3(*sm)},{_fixed3(*sa)},{_fixed3(*wm)},{_fixed3(*wa)}")
+    return "\n".join(out) + "\n"
+
+
+def format_ratio_table(rows) -> str:
+    """opmodel.hpp:123-141 (fixed-width text table)."""
+    lw, cw = 18, 10
+    nm = rows[0][1] if rows else 0
+    lines = [" " * lw + " |" + "Strassen".rjust(2 * cw) + " |" + "Winograd".rjust(2 * cw),
+             f"n_min = {nm}".ljust(lw) + " |" + "Add & Sub".rjust(cw) + "Mul".rjust(cw) + " |" +
+             "Add & Sub".rjust(cw) + "Mul".rjust(cw),
+             "-" * lw + "-+" + "-" * (2 * cw) + "-+" + "-" * (2 * cw)]
+    for (m, l, n), _, sm, sa, wm, wa in rows:
+        label = f"{m} x {n}" if m == l == n else f"{m} x {l} x {n}"
+        lines.append(label.rjust(lw) + " |" + _fixed3(*sa).rjust(cw) + _fixed3(*sm).rjust(cw) + " |" +
+                     _fixed3(*wa).rjust(cw) + _fixed3(*wm).rjust(cw))
+    return "\n".join(lines) + "\n"
+
+
+def parse_sizes(tokens) -> list:
+    """mpmm_bench.cpp:23-45: integers N (an N x N x N product) and ranges a..b expanding to
+    2^k-1, 2^k, 2^k+1 within [a, b]; sorted, unique."""
+    sizes = set()
+    for tok in tokens:
+        if ".." in tok:
+            lo, hi = (int(x) for x in tok.split("..", 1))
+            if lo == 0 or hi < lo:
+                raise DomainError(f"bad size range '{tok}'")
+            k = 1
+            while (1 << k) <= hi + 1:
+                for dd in (-1, 0, 1):
+                    v = (1 << k) + dd
+                    if lo <= v <= hi:
+                        sizes.add(v)
+                k += 1
+        else:
+            sizes.add(int(tok))
+    if not sizes:
+        raise DomainError("no sizes given")
+    return [(s, s, s) for s in sorted(sizes)]

@@ -1,6 +1,7 @@
-"""GPU drop-in for the reference CLI's `matmul` and `lu` subcommands
-(mpmm_bench.cpp:66-79, 137-240): same flags, same CSV, same exit codes
-(1 error, 2 singular pivot in the sweep, 3 I/O).
+"""GPU drop-in for the reference CLI (mpmm_bench.cpp:66-240): `matmul` and `lu` run on
+the GPU and print the reference's CSV; `opcount` (analytic ratios) and `gen` (matrix
+text files) are host-side.  Same flags, same exit codes (1 error, 2 singular pivot in
+the sweep, 3 I/O).
 
     python -m paper_1410_1599_b200.cli matmul --algo all --m 256 --l 256 --n 256 --bits 128 --nmin 32
     python -m paper_1410_1599_b200.cli lu --matrix random --n 128 --bits 256 --kernel winograd \\
@@ -47,9 +48,22 @@ def main(argv=None) -> int:
     lu.add_argument("--seed", type=int, default=1)
     lu.add_argument("--verbose", action="store_true")
     lu.add_argument("--csv", default="")
+    oc = sub.add_parser("opcount", help="analytic operation-count ratios")
+    oc.add_argument("--sizes", required=True, help="sizes: integers and/or a..b ranges, comma-separated")
+    oc.add_argument("--nmin", type=int, default=32)
+    oc.add_argument("--format", default="table", choices=["table", "csv"])
+    gn = sub.add_parser("gen", help="write a generated matrix as text")
+    gn.add_argument("--kind", default="lotkin", choices=["bench-a", "bench-b", "random", "lotkin"])
+    gn.add_argument("--m", type=int, default=4)
+    gn.add_argument("--l", type=int, default=4)
+    gn.add_argument("--n", type=int, default=4)
+    gn.add_argument("--bits", type=int, default=128)
+    gn.add_argument("--seed", type=int, default=1)
+    gn.add_argument("--out", default="")
     a = ap.parse_args(argv)
 
     from . import benchdrv as B
+    from .codec import IoError
     from .mpmm import Error, SingularError, parse_algorithm
 
     def emit(rows, path):
@@ -59,6 +73,32 @@ def main(argv=None) -> int:
             B.print_csv(sys.stdout, rows)
 
     try:
+        if a.cmd == "opcount":
+            rows = B.ratio_table(B.parse_sizes([t for t in a.sizes.split(",") if t]), a.nmin)
+            sys.stdout.write(B.format_ratio_table(rows) if a.format == "table" else B.format_ratio_csv(rows))
+            return 0
+        if a.cmd == "gen":
+            from . import codec
+            from .matgen import gen_random
+            from .mpmm import PrecisionContext
+            ctx = PrecisionContext(a.bits)
+            if a.kind == "bench-a":
+                x = B.gen_bench_pair(a.m, a.l, 1, ctx)[0]
+            elif a.kind == "bench-b":
+                x = B.gen_bench_pair(1, a.l, a.n, ctx)[1]
+            elif a.kind == "random":
+                x = gen_random(a.m, a.n, a.seed, ctx)
+            else:
+                x = B.gen_lotkin(a.n, ctx)
+            if not a.out:
+                codec.write_matrix(sys.stdout, x)
+                return 0
+            try:
+                with open(a.out, "w") as f:
+                    codec.write_matrix(f, x)
+            except OSError as e:
+                raise IOError(f"cannot open output file: {a.out}") from e
+            return 0
         if a.cmd == "matmul":
             algos = [parse_algorithm(k) for k in KINDS] if a.algo == "all" else [parse_algorithm(a.algo)]
             q = B.MatmulRequest(algos, a.m, a.l, a.n, a.bits, a.nmin, a.ref_bits_multiplier, a.verbose)
@@ -77,13 +117,12 @@ def main(argv=None) -> int:
     except SingularError as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_SINGULAR
-    except (IOError, OSError) as e:
+    except (IOError, OSError, IoError) as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_IO
     except Exception as e:  # noqa: BLE001 -- mirrors the reference's catch-all
         print(f"error: {e}", file=sys.stderr)
         return EXIT_ERROR
-
 
 if __name__ == "__main__":
     sys.exit(main())

@@ -155,6 +155,13 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b,
                    mpgpu_mat* x, int exact, int64_t* zero_pivot);
 
+/* lu_solve for r right-hand sides at once (rows of the r x n matrix Bt; solutions in the
+ * rows of Xt), one CTA per right-hand side -- e.g. inverse() (blocklu.hpp:263-281) */
+int mpgpu_lu_solve_many(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* Bt,
+                        mpgpu_mat* Xt, int exact, int64_t* zero_pivot);
+/* dst = RN(src) at dst->prec (mpfr_set between precisions, blocklu.hpp:266-270); same shape */
+int mpgpu_convert(mpgpu_handle* h, const mpgpu_mat* src, mpgpu_mat* dst);
+
 /* ---- accuracy metrics (device-side; bench.hpp:145-147, 217, 238) ---------
  * Results are returned as host SoA scalars at the reference's precision, limb planes
  * of nlimbs_out = ref->nlimbs limbs (limbs[k * count + e] is limb k of result e).

@@ -444,3 +444,21 @@ def ratio_table(sizes, n_min, fmt="table"):
     _check(ref().ref_ratio_table(0 if fmt == "table" else 1, arr, len(sizes), C.c_int64(n_min), buf,
                                  C.c_int64(len(buf))))
     return buf.value.decode()
+
+
+def inverse(a, bits):
+    n = a.rows()
+    x = OMat(n, n, bits)
+    piv = C.c_int64(0)
+    _check(ref().ref_inverse(C.c_long(a.bits()), a.nlimbs, C.c_int64(n), *_soa(a), C.c_long(bits), x.nlimbs,
+                             *_soa(x), C.byref(piv)), piv.value)
+    return x
+
+
+def cond_one(a, hi_bits=0):
+    bits = hi_bits or min(2 * a.bits() + 64, 1 << 20)
+    out = OMat(1, 1, bits)
+    piv = C.c_int64(0)
+    _check(ref().ref_cond_one(C.c_long(a.bits()), a.nlimbs, C.c_int64(a.rows()), *_soa(a), C.c_long(hi_bits),
+                              out.nlimbs, *_soa(out), C.byref(piv)), piv.value)
+    return out

@@ -540,4 +540,24 @@ int ref_ratio_table(int format, const std::int64_t* sizes, int count, std::int64
   });
 }
 
+// inverse / cond_one (blocklu.hpp:261-301)
+int ref_inverse(long pa, int La, std::int64_t n, const std::uint32_t* al, const std::int32_t* ae,
+                const std::uint8_t* as, long pc, int Lc, std::uint32_t* xl, std::int32_t* xe, std::uint8_t* xs,
+                std::int64_t* pivot) {
+  return guarded([&] { return store(inverse(load(n, n, pa, La, al, ae, as), PrecisionContext(pc)), Lc, xl, xe, xs); },
+                 pivot);
+}
+
+int ref_cond_one(long pa, int La, std::int64_t n, const std::uint32_t* al, const std::int32_t* ae,
+                 const std::uint8_t* as, long phi, int Lo, std::uint32_t* ol, std::int32_t* oe, std::uint8_t* os,
+                 std::int64_t* pivot) {
+  return guarded([&] {
+    Matrix a = load(n, n, pa, La, al, ae, as);
+    Scalar c = phi > 0 ? cond_one(a, PrecisionContext(phi)) : cond_one(a);
+    Matrix out(1, 1, PrecisionContext(mpfr_get_prec(c.raw())));
+    out.at(0, 0) = c;
+    return store(out, Lo, ol, oe, os);
+  }, pivot);
+}
+
 }  // extern "C"

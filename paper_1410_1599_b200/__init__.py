@@ -8,7 +8,8 @@ from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix
                    lu_blocked, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
                    record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
                    solve_columnwise, sub, vec_op, UndefinedMetricError, RelErrorStats, SolutionError,
-                   max_rel_error, max_rel_error_solution, one_norm)
+                   max_rel_error, max_rel_error_solution, one_norm, convert, lu_solve_many,
+                   inverse, cond_one)
 from .matgen import Prng64, from_ints, gen_random, gen_scaled, gen_uniform_full, to_fractions
 from .codec import IoError, ParseError, from_hex, read_matrix, to_hex, write_matrix
 from .benchdrv import (CSV_HEADER, BenchRecord, LUOutcome, LURequest, MatmulRequest, append_csv, bench_reference,

@@ -71,6 +71,8 @@ _SIGS = {
     "mpgpu_recursion_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int,
                                        C.POINTER(C.c_int)]),
     "mpgpu_gen": (C.c_int, [C.c_int, C.c_int64, C.c_uint64, C.c_int32, vp, vp, vp, C.c_int32]),
+    "mpgpu_lu_solve_many": (C.c_int, [vp, MatP, vp, MatP, MatP, C.c_int, i64p]),
+    "mpgpu_convert": (C.c_int, [vp, MatP, MatP]),
     "mpgpu_max_rel_error": (C.c_int, [vp, MatP, MatP, vp, vp, vp, i64p]),
     "mpgpu_solution_error": (C.c_int, [vp, MatP, MatP, vp, vp, vp, i64p]),
     "mpgpu_one_norm": (C.c_int, [vp, MatP, vp, vp, vp]),

@@ -1151,14 +1151,10 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
   return rc;
 }
 
-int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
-                   int exact, int64_t* zero_pivot) {
-  if (!h || !F || !b || !x) return MPGPU_ERR_DOMAIN;
-  if (zero_pivot) *zero_pivot = 0;
-  if (int r = compute_range(h, {F, b, x})) return r;
+namespace {
+int lu_solve_impl(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
+                  int exact, int64_t* zero_pivot, int64_t nrhs) {
   const int64_t n = F->rows;
-  if (F->rows != F->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: factors must be square");
-  if (b->rows * b->cols != n || x->rows * x->cols != n) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: length mismatch");
   if (b->prec != F->prec || x->prec != F->prec) return fail(h, MPGPU_ERR_DOMAIN, "lu_solve: mixed precisions");
   std::lock_guard<std::mutex> lk(h->mu);
   cudaSetDevice(h->device);
@@ -1172,9 +1168,9 @@ int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, cons
   const int sh = 32 * F->nlimbs - F->prec;
   int rc = dispatch_L(F->nlimbs, [&](auto Lc) -> int {
     constexpr int L = decltype(Lc)::value;
-    CUDA_TRY(h, scratch.alloc(h, sizeof(uint32_t) * rec_stride(L) * 2 * n));
+    CUDA_TRY(h, scratch.alloc(h, sizeof(uint32_t) * rec_stride(L) * 2 * n * nrhs));
     mpg::launch_lu_solve<L>(F->rec, n, piv ? static_cast<const int64_t*>(dpiv.p) : nullptr, b->rec, x->rec,
-                            scratch.u32(), sh, h->d_err, zp, exact, h->stream);
+                            scratch.u32(), sh, h->d_err, zp, exact, nrhs, h->stream);
     return 0;
   });
   if (rc) return rc;
@@ -1186,6 +1182,51 @@ int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, cons
     return fail(h, MPGPU_ERR_SINGULAR, "zero pivot at index %lld", (long long)zpv);
   }
   return rc;
+}
+}  // namespace
+
+int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
+                   int exact, int64_t* zero_pivot) {
+  if (!h || !F || !b || !x) return MPGPU_ERR_DOMAIN;
+  if (zero_pivot) *zero_pivot = 0;
+  if (int r = compute_range(h, {F, b, x})) return r;
+  const int64_t n = F->rows;
+  if (F->rows != F->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: factors must be square");
+  if (b->rows * b->cols != n || x->rows * x->cols != n) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: length mismatch");
+  return lu_solve_impl(h, F, piv, b, x, exact, zero_pivot, 1);
+}
+
+int mpgpu_lu_solve_many(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* Bt, mpgpu_mat* Xt,
+                        int exact, int64_t* zero_pivot) {
+  if (!h || !F || !Bt || !Xt) return MPGPU_ERR_DOMAIN;
+  if (zero_pivot) *zero_pivot = 0;
+  if (int r = compute_range(h, {F, Bt, Xt})) return r;
+  const int64_t n = F->rows;
+  if (F->rows != F->cols) return fail(h, MPGPU_ERR_DIMENSION, "lu_solve: factors must be square");
+  if (Bt->cols != n || Xt->cols != n || Xt->rows != Bt->rows)
+    return fail(h, MPGPU_ERR_DIMENSION, "lu_solve_many: right-hand sides must be r x n (one per row)");
+  if (Bt->ld != Bt->cols || Xt->ld != Xt->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "lu_solve_many: strided views are not supported");
+  return lu_solve_impl(h, F, piv, Bt, Xt, exact, zero_pivot, Bt->rows);
+}
+
+int mpgpu_convert(mpgpu_handle* h, const mpgpu_mat* src, mpgpu_mat* dst) {
+  if (!h || !src || !dst) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {dst})) return r;
+  if (src->rows != dst->rows || src->cols != dst->cols)
+    return fail(h, MPGPU_ERR_DIMENSION, "convert: shape mismatch");
+  if (src->ld != src->cols || dst->ld != dst->cols) return fail(h, MPGPU_ERR_DIMENSION, "convert: strided view");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * dst->nlimbs - dst->prec;
+  int rc = dispatch_L(dst->nlimbs, [&](auto Lc) {
+    mpg::launch_convert<decltype(Lc)::value>(src->rec, src->nlimbs, src->rows * src->cols, dst->rec, sh, h->d_err,
+                                             h->stream);
+    return 0;
+  });
+  if (rc) return rc;
+  return check_err(h);
 }
 
 int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out5) {

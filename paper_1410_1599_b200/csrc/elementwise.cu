@@ -202,6 +202,36 @@ __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ p
   }
 }
 
+// mpfr_set into another precision: round the ls-limb source mantissa to 32L - sh bits
+template <int L>
+__global__ void convert_kernel(const uint32_t* __restrict__ src, int ls, int ss, int64_t N,
+                               uint32_t* __restrict__ dst, int sh, uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* r = src + e * ss;
+    MP<L> z;
+    z.e = (int32_t)r[ls];
+    z.s = r[ls + 1];
+    uint32_t g = 0, st = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int q = ls - L + k;  // source limb feeding destination limb k (aligned at the top)
+      z.m[k] = q >= 0 ? r[q] : 0u;
+    }
+    if (ls > L) {
+      g = r[ls - L - 1];
+      for (int q = 0; q < ls - L - 1; ++q) st |= r[q];
+    }
+    if (z.e != EXP_ZERO) {
+      int32_t ex = z.e;
+      round_p<L>(z.m, g, st, sh, ex);
+      z.e = ex;
+      if (exp_out_of_range(z.e)) atomicOr(err, ERR_EXP_RANGE);
+    }
+    store_rec<L>(dst + e * S, z);
+  }
+}
+
 template <int L>
 __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r, int c, const MP<L>& x,
                                          uint32_t* err) {
@@ -379,6 +409,11 @@ void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd,
   copy2d_kernel<L><<<grid_for(total), NT, 0, st>>>(src, lds, dst, ldd, rows, cols);
 }
 
+template <int L>
+void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int sh, uint32_t* err, cudaStream_t st) {
+  convert_kernel<L><<<grid_for(N), NT, 0, st>>>(src, ls, rec_stride(ls), N, dst, sh, err);
+}
+
 #define MPG_INST(L)                                                                                     \
   template void launch_soa2rec<L>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t,   \
                                   uint32_t*, cudaStream_t);                                             \
@@ -393,6 +428,7 @@ void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd,
   template void launch_postadd<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, uint32_t*, int,   \
                                   uint32_t*, cudaStream_t);                                             \
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
+  template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);
 // 64 limbs (p <= 2048): storage only -- references of the accuracy metrics (metrics.cu)
 template void launch_soa2rec<64>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t, uint32_t*,

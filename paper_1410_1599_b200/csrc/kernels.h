@@ -117,11 +117,12 @@ template <int L>
 void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0, int64_t w, int sh,
                          cudaStream_t st);
 
-// Ly = Pb, Ux = y on packed factors (blocklu.hpp:215-245); scratch: 2n records
+// Ly = Pb, Ux = y on packed factors (blocklu.hpp:215-245) for nrhs right-hand sides
+// (one CTA each; b, x: nrhs x n records); scratch: 2n records per right-hand side
 template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b,
                      uint32_t* x, uint32_t* scratch, int sh, uint32_t* err, int64_t* zp,
-                     int exact, cudaStream_t st);
+                     int exact, int64_t nrhs, cudaStream_t st);
 
 // C(view, ldc) = RN(C - T) for a dense rows x cols T (LU Schur subtraction)
 template <int L>
@@ -147,5 +148,10 @@ void launch_colsum_abs(const uint32_t* A, int64_t ld, int rows, int cols, int sh
 template <int L>
 void launch_reduce3(const uint32_t* A, const uint32_t* B, int64_t N, uint32_t* out3, uint32_t* scratch,
                     cudaStream_t st);
+
+// RN conversion between precisions (mpfr_set, blocklu.hpp:266-270): records of ls limbs
+// (stride rec_stride(ls)) -> records of L limbs rounded to 32L - sh bits
+template <int L>
+void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int sh, uint32_t* err, cudaStream_t st);
 
 }  // namespace mpg

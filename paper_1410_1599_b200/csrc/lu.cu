@@ -293,6 +293,11 @@ __global__ void __launch_bounds__(NT) lu_solve_kernel(const uint32_t* f, int64_t
                                                       int exact) {
   constexpr int S = rec_stride(L);
   constexpr int CH = S / 4;
+  // one CTA per right-hand side (blockIdx.x): its b, x and 2n scratch records
+  b += (int64_t)blockIdx.x * n * S;
+  x += (int64_t)blockIdx.x * n * S;
+  y += (int64_t)blockIdx.x * 2 * n * S;
+  tmp = y + n * S;
   // y = b
   for (int64_t t = threadIdx.x; t < n * CH; t += blockDim.x)
     reinterpret_cast<uint4*>(y)[t] = reinterpret_cast<const uint4*>(b)[t];
@@ -627,9 +632,9 @@ void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c
 
 template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b, uint32_t* x,
-                     uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, int exact, cudaStream_t st) {
-  constexpr int S = rec_stride(L);
-  lu_solve_kernel<L><<<1, NT, 0, st>>>(f, n, piv_dev, b, x, scratch, scratch + n * S, sh, err, zp, exact);
+                     uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, int exact, int64_t nrhs,
+                     cudaStream_t st) {
+  lu_solve_kernel<L><<<(unsigned)nrhs, NT, 0, st>>>(f, n, piv_dev, b, x, scratch, nullptr, sh, err, zp, exact);
 }
 
 #define MPG_LU_INST(L)                                                                                      \
@@ -644,7 +649,7 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
   template int launch_lu_panel_coop<L>(uint32_t*, int64_t, int64_t, int64_t, int64_t, int, int64_t*, int64_t*, int, \
                                        uint64_t*, int64_t*, int, cudaStream_t);                                      \
   template void launch_lu_solve<L>(const uint32_t*, int64_t, const int64_t*, const uint32_t*, uint32_t*,        \
-                                   uint32_t*, int, uint32_t*, int64_t*, int, cudaStream_t);
+                                   uint32_t*, int, uint32_t*, int64_t*, int, int64_t, cudaStream_t);
 MPG_LU_INST(1)
 MPG_LU_INST(2)
 MPG_LU_INST(4)

@@ -850,3 +850,81 @@ def one_norm(a) -> Matrix:
         if fa:
             da.free()
     return _scalars(ol, oe, os_, a.bits(), L)[0]
+
+
+# ---------------------------------------------------------------------------
+# precision conversion, multi-RHS solves, inverse and 1-norm condition number
+# (blocklu.hpp:261-301; SURVEY.md §8f rank 3 within the device precision range)
+# ---------------------------------------------------------------------------
+
+
+def convert(a, ctx: PrecisionContext) -> "DeviceMatrix":
+    """mpfr_set of every element into ctx (round to nearest), on the device."""
+    da, fa = _dev(a)
+    out = DeviceMatrix(da.rows(), da.cols(), ctx)
+    try:
+        _raise(out._h, _L.lib.mpgpu_convert(out._h, C.byref(da.m), C.byref(out.m)))
+    except Exception:
+        out.free()
+        raise
+    finally:
+        if fa:
+            da.free()
+    return out
+
+
+def lu_solve_many(f: LUFactors, bt: Matrix, ctx: PrecisionContext, exact: bool = True) -> Matrix:
+    """lu_solve (blocklu.hpp:215-245) for every row of the r x n matrix bt at once."""
+    n = f.n
+    if bt.cols() != n:
+        raise DimensionError("lu_solve_many: right-hand sides must be the rows of an r x n matrix")
+    df = f.packed.to_device()
+    db = bt.to_device()
+    dx = DeviceMatrix(bt.rows(), n, ctx)
+    zp = C.c_int64(0)
+    piv = None if f.piv is None else np.ascontiguousarray(f.piv, np.int64)
+    rc = _L.lib.mpgpu_lu_solve_many(df._h, C.byref(df.m), None if piv is None else _ptr(piv), C.byref(db.m),
+                                    C.byref(dx.m), 1 if exact else 0, C.byref(zp))
+    try:
+        _raise(df._h, rc, zp.value)
+        return dx.download()
+    finally:
+        df.free()
+        db.free()
+        dx.free()
+
+
+def _transpose(x: Matrix) -> Matrix:
+    r, c = x.rows(), x.cols()
+    idx = np.arange(r * c).reshape(r, c).T.reshape(-1)
+    return Matrix(c, r, x.ctx(), x.limbs[:, idx], x.exp[idx], x.sign[idx])
+
+
+def inverse(a: Matrix, ctx: PrecisionContext) -> Matrix:
+    """blocklu.hpp:263-281: a copied into ctx, lu_columnwise, one lu_solve per unit
+    vector (all n at once on the device), same operation order (bit-exact)."""
+    if a.rows() != a.cols():
+        raise DimensionError("inverse: matrix must be square")
+    n = a.rows()
+    dahi = convert(a, ctx)
+    ahi = dahi.download()
+    dahi.free()
+    f = lu_columnwise(ahi)
+    from .matgen import from_ints
+    eye = from_ints(np.eye(n, dtype=np.int64), ctx, n, n)
+    xt = lu_solve_many(f, eye, ctx)  # row j = the solution for e_j = column j of the inverse
+    return _transpose(xt)
+
+
+def cond_one(a: Matrix, ctx_hi: Optional[PrecisionContext] = None) -> Matrix:
+    """blocklu.hpp:285-301: ||A||_1 * ||A^-1||_1 with everything at ctx_hi (default
+    min(2 bits + 64, max_bits)); 1x1 Matrix.  Device arithmetic: ctx_hi <= 1024 bits."""
+    if ctx_hi is None:
+        ctx_hi = PrecisionContext(min(2 * a.bits() + 64, PrecisionContext.max_bits))
+    dahi = convert(a, ctx_hi)
+    try:
+        na = one_norm(dahi)
+    finally:
+        dahi.free()
+    ni = one_norm(inverse(a, ctx_hi))
+    return vec_op(2, na, ni)

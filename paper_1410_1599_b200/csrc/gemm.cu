@@ -16,6 +16,8 @@
 // Limb products are IMAD / IMAD.HI on the FMA pipe (mp_arith.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "mp_arith.cuh"
 
@@ -230,8 +232,16 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
                          (int)smem);
     configured = true;
   }
-  dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, g.batch);
-  kern<<<grid, TM * TN, smem, st>>>(g);
+  // grid.z is limited to 65535: deep recursions (7^d leaves) launch in batch chunks
+  for (int z0 = 0; z0 < g.batch; z0 += 65535) {
+    GemmArgs gz = g;
+    gz.batch = std::min(65535, g.batch - z0);
+    gz.A += (int64_t)z0 * g.strideA * S;
+    gz.B += (int64_t)z0 * g.strideB * S;
+    gz.C += (int64_t)z0 * g.strideC * S;
+    dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, gz.batch);
+    kern<<<grid, TM * TN, smem, st>>>(gz);
+  }
 }
 
 template void launch_gemm<1>(const GemmArgs&, cudaStream_t);

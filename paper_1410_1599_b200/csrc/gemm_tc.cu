@@ -28,6 +28,8 @@
 //                         as the IMAD kernel, so the rounding sequence is identical.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -411,8 +413,16 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
       return false;
     configured = true;
   }
-  dim3 grid((g.n + CF::JT - 1) / CF::JT, (g.m + CF::IT - 1) / CF::IT, g.batch);
-  kern<<<grid, CF::NT, CF::SMEM, st>>>(g);
+  constexpr int S = rec_stride(L);
+  for (int z0 = 0; z0 < g.batch; z0 += 65535) {  // grid.z limit
+    GemmArgs gz = g;
+    gz.batch = std::min(65535, g.batch - z0);
+    gz.A += (int64_t)z0 * g.strideA * S;
+    gz.B += (int64_t)z0 * g.strideB * S;
+    gz.C += (int64_t)z0 * g.strideC * S;
+    dim3 grid((g.n + CF::JT - 1) / CF::JT, (g.m + CF::IT - 1) / CF::IT, gz.batch);
+    kern<<<grid, CF::NT, CF::SMEM, st>>>(gz);
+  }
   return true;
 }
 

@@ -189,3 +189,16 @@ def test_randomized_shapes_precisions_algorithms(P, O):
         want, wops = O.gemm(alg, param if alg != "simple" else 0, O.OMat.of(a), O.OMat.of(b))
         assert P.identical(c, want), (m, l, n, bits, alg, param)
         assert (ops.mul, ops.addsub) == wops
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg", ["strassen", "winograd"])
+def test_deep_recursion_more_leaves_than_grid_z(P, O, alg):
+    # n_min 1 at n = 100: depth 7, 7^7 = 823543 leaves > 65535 (grid.z limit): the leaf
+    # launch is split into batch chunks
+    ctx = P.PrecisionContext(64)
+    a = P.gen_uniform_full(100, 100, 3, ctx)
+    b = P.gen_uniform_full(100, 100, 4, ctx)
+    c = _run(P, alg, 1, a, b, ctx, P.OpCounter())
+    want, _ = O.gemm(alg, 1, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)

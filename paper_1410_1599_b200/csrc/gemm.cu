@@ -56,6 +56,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+#ifndef MPG_KK_UNROLL_8
+#define MPG_KK_UNROLL_8 2  // measured: 2 beats 1 and 4 at 256 bits (and loses at L >= 16)
+#endif
+
 #ifndef MPG_TK_8
 #define MPG_TK_8 16
 #endif
@@ -72,26 +76,32 @@ struct GemmCfg;
 template <>
 struct GemmCfg<1> {
   static constexpr int MINB = MPG_MINB_1, TM = 16, TN = 16, TK = 16, U = 1;
+  static constexpr int KU = 1;
 };
 template <>
 struct GemmCfg<2> {
   static constexpr int MINB = MPG_MINB_2, TM = 16, TN = 16, TK = 16, U = 1;
+  static constexpr int KU = 1;
 };
 template <>
 struct GemmCfg<4> {
   static constexpr int MINB = MPG_MINB_4, TM = 16, TN = 16, TK = 16, U = 1;
+  static constexpr int KU = 1;
 };
 template <>
 struct GemmCfg<8> {
   static constexpr int MINB = MPG_MINB_8, TM = 16, TN = 16, TK = MPG_TK_8, U = MPG_U_8;
+  static constexpr int KU = MPG_KK_UNROLL_8;
 };
 template <>
 struct GemmCfg<16> {
   static constexpr int MINB = MPG_MINB_16, TM = 8, TN = 16, TK = 8, U = 1;
+  static constexpr int KU = 1;
 };
 template <>
 struct GemmCfg<32> {
   static constexpr int MINB = MPG_MINB_32, TM = MPG_TM_32, TN = 16, TK = MPG_TK_32, U = 1;
+  static constexpr int KU = 1;
 };
 
 template <int L, int TM, int TN, int TK, int U, bool FOLD>
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
       const uint32_t* a_rows = sA + (kt & 1) * A_WORDS + ty * TK * S;
       const uint32_t* b_cols = sB + (kt & 1) * B_WORDS + tx * S;
       const int kend = min(TK, g.l - kt * TK);
-#pragma unroll 1
+#pragma unroll GemmCfg<L>::KU
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
         if (FOLD && k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P

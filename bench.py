@@ -11,8 +11,9 @@ resident operands.  --algo block|strassen|winograd|simple selects the other arms
 
 N > 1 (torchrun): the 7^d leaf products are sharded across ranks (each rank does
 the pre-additions for its own leaves from replicated A and B, no data-path
-collective on the leaf work); the post-additions run after an all-gather of the
-leaf products.  Timing: CUDA events around each step
+collective on the leaf work); one all-to-all moves the unit products' row slices
+to their owners and each rank post-adds its own rows of C (see DESIGN.md
+"Multi-GPU").  Timing: CUDA events around each step
 on the launching stream, an L2 flush (256 MiB write) between steps, barrier +
 synchronize on both sides, max over ranks.
 """
@@ -49,9 +50,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--shard", choices=["auto", "replicas"], default="auto",
-                    help="N>1: auto = leaf shards (Strassen/Winograd) or row shards (Simple/Block) "
-                         "with one all-gather (strong scaling); replicas = independent copies (weak)")
+    ap.add_argument("--shard", choices=["auto", "gather", "replicas"], default="auto",
+                    help="N>1: auto = leaf shards with one all-to-all and a row-owned combine "
+                         "(Strassen/Winograd) or row shards (Simple/Block) (strong scaling); gather = "
+                         "leaf shards + all-gather + replicated combine; replicas = independent copies (weak)")
     return ap.parse_args()
 
 

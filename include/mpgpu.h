@@ -205,6 +205,18 @@ int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat*
                       mpgpu_stats* stats);
 int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
                        const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats);
+/* Row-owned combine: node_products holds (at least) rows [row_lo, row_hi) of every
+ * level-(d - up_levels) node product; only the rows of C (and of every intermediate
+ * level) that derive from them are computed -- a level-t row r comes from child row r
+ * or r - m_{t+1}, so ownership propagates through the pad/halve index map.  Ranks that
+ * own disjoint unit-row ranges (exchanged with one all-to-all) together produce all of
+ * C without replicated post-additions. */
+int mpgpu_fast_combine_rows(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
+                            const uint32_t* node_products, int64_t row_lo, int64_t row_hi, mpgpu_mat* C,
+                            mpgpu_stats* stats);
+/* device-to-device 2D copy on the handle's stream (packing row slices for the all-to-all) */
+int mpgpu_copy_device_2d(mpgpu_handle* h, void* dst, size_t dpitch, const void* src, size_t spitch,
+                         size_t width, size_t height);
 
 /* ---- host-side model / plan / inputs ------------------------------------ */
 /* count_fast (opmodel.hpp:30-44); SIMPLE / BLOCK give count_simple */

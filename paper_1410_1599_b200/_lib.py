@@ -67,6 +67,9 @@ _SIGS = {
     "mpgpu_fast_leaves": (C.c_int, [vp, C.c_int, C.c_int64, MatP, MatP, C.c_int, C.c_int64, C.c_int64, vp,
                                     StatsP]),
     "mpgpu_fast_combine": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, MatP, StatsP]),
+    "mpgpu_fast_combine_rows": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, C.c_int64, C.c_int64,
+                                          MatP, StatsP]),
+    "mpgpu_copy_device_2d": (C.c_int, [vp, vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t]),
     "mpgpu_count_fast": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, u64p]),
     "mpgpu_recursion_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int,
                                        C.POINTER(C.c_int)]),

@@ -530,9 +530,30 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
   return MPGPU_OK;
 }
 
+// Rows of each level's node products produced from the unit-level rows [lo, hi) (the
+// row-owned combine): a level-t row r comes from child row r (top quadrants) or
+// r - m_{t+1} (bottom), so ownership propagates up through the pad/halve index map.
+// owned[t] lists the owned rows of a level-t node, t = 0 .. il.
+std::vector<std::vector<int>> owned_rows(const std::vector<Level>& lv, int il, int64_t lo, int64_t hi) {
+  std::vector<std::vector<int>> owned(il + 1);
+  for (int64_t r = lo; r < hi && r < lv[il].m; ++r) owned[il].push_back((int)r);
+  for (int t = il - 1; t >= 0; --t) {
+    const int64_t hm = lv[t + 1].m;
+    std::vector<char> mark(lv[t].m, 0);
+    for (int rc : owned[t + 1]) {
+      if (rc < lv[t].m) mark[rc] = 1;
+      if (rc + hm < lv[t].m) mark[rc + hm] = 1;
+    }
+    for (int64_t r = 0; r < lv[t].m; ++r)
+      if (mark[r]) owned[t].push_back((int)r);
+  }
+  return owned;
+}
+
 template <int L>
 int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* leafprods, int in_up, int64_t m,
-                     int64_t l, int64_t n, uint32_t* C, int64_t ldc, int sh, mpgpu_stats* stats) {
+                     int64_t l, int64_t n, uint32_t* C, int64_t ldc, int sh, mpgpu_stats* stats, int64_t row_lo = 0,
+                     int64_t row_hi = -1) {
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   Timer tpost(stats != nullptr, st);
@@ -541,6 +562,23 @@ int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* l
   if (d == 0) return fail(h, MPGPU_ERR_DOMAIN, "fast_combine: the product is a base case (depth 0)");
   if (in_up < 0 || in_up >= d) return fail(h, MPGPU_ERR_DIMENSION, "fast_combine: bad input level");
   const int il = d - in_up;  // level of the given node products
+  if (row_hi < 0) row_hi = lv[il].m;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > lv[il].m)
+    return fail(h, MPGPU_ERR_DIMENSION, "fast_combine: bad unit row range");
+  const bool partial = row_lo > 0 || row_hi < lv[il].m;
+  // device lists of the owned child rows per level (row-owned combine only)
+  std::vector<DevBuf> rowbuf(il + 1);
+  std::vector<int> nrows(il + 1, 0);
+  if (partial) {
+    const auto owned = owned_rows(lv, il, row_lo, row_hi);
+    for (int t = 1; t <= il; ++t) {
+      nrows[t] = (int)owned[t].size();
+      CUDA_TRY(h, rowbuf[t].alloc(h, sizeof(int) * (owned[t].size() + 1)));
+      if (!owned[t].empty())
+        CUDA_TRY(h, cudaMemcpyAsync(rowbuf[t].p, owned[t].data(), sizeof(int) * owned[t].size(),
+                                    cudaMemcpyHostToDevice, st));
+    }
+  }
   int64_t nodes = 1;
   for (int i = 0; i < il; ++i) nodes *= 7;
   std::vector<DevBuf> prod(d + 1);
@@ -560,12 +598,13 @@ int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* l
       CUDA_TRY(h, prod[lev].alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
       dst = prod[lev].u32();
     }
-    mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st);
+    mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st,
+                           partial ? static_cast<const int*>(rowbuf[lev + 1].p) : nullptr, nrows[lev + 1]);
     ++launches;
     if (lev + 1 < il) prod[lev + 1].release();
     cur = dst;
   }
-  if (top.p) {
+  if (top.p) {  // (a strided C: copy the whole window -- rows not owned are copied unset)
     mpg::launch_copy2d<L>(top.u32(), n, C, ldc, (int)m, (int)n, st);
     ++launches;
   }
@@ -1285,6 +1324,38 @@ int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int 
   });
   if (rc) return rc;
   return check_err(h);
+}
+
+int mpgpu_fast_combine_rows(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
+                            const uint32_t* node_products, int64_t row_lo, int64_t row_hi, mpgpu_mat* C,
+                            mpgpu_stats* stats) {
+  TimerGuard timer_guard;
+  if (!h || !C || !node_products) return MPGPU_ERR_DOMAIN;
+  if (int r = compute_range(h, {C})) return r;
+  if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
+    return fail(h, MPGPU_ERR_DOMAIN, "fast_mul: algorithm must be strassen or winograd");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  if (stats) std::memset(stats, 0, sizeof *stats);
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
+  const int sh = 32 * C->nlimbs - C->prec;
+  int rc = dispatch_L(C->nlimbs, [&](auto Lc) {
+    return run_fast_combine<decltype(Lc)::value>(h, algo, n_min, node_products, up_levels, C->rows, l, C->cols,
+                                                 C->rec, C->ld, sh, stats, row_lo, row_hi);
+  });
+  if (rc) return rc;
+  return check_err(h);
+}
+
+int mpgpu_copy_device_2d(mpgpu_handle* h, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                         size_t height) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  if (width == 0 || height == 0) return MPGPU_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToDevice, h->stream));
+  return MPGPU_OK;
 }
 
 // ---- accuracy metrics (metrics.cu) -------------------------------------------

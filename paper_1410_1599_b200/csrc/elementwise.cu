@@ -244,16 +244,20 @@ __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r,
 template <int L>
 __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
                                int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
-                               int sh, uint32_t* err) {
+                               int sh, uint32_t* err, const int* __restrict__ rowlist, int nrows) {
   constexpr int S = rec_stride(L);
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
   const int64_t per = (int64_t)hr * hc;
-  const int64_t total = per * nodes;
+  // rowlist: only these child rows (row-owned combine of the multi-GPU path)
+  const int64_t per_iter = (rowlist ? (int64_t)nrows : (int64_t)hr) * hc;
+  const int64_t total = per_iter * nodes;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t node = t / per;
-    const int64_t e = t - node * per;
-    const int r = (int)(e / hc), c = (int)(e - (int64_t)r * hc);
+    const int64_t node = t / per_iter;
+    const int64_t ei = t - node * per_iter;
+    const int ri = (int)(ei / hc), c = (int)(ei - (int64_t)ri * hc);
+    const int r = rowlist ? rowlist[ri] : ri;
+    const int64_t e = (int64_t)r * hc + c;
     const uint32_t* M = children + (node * 7 * per + e) * S;
     const int64_t cs = per * S;
     uint32_t* P = parent + node * (int64_t)rows * cols * S;
@@ -397,10 +401,12 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 }
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
-                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st) {
-  const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist,
+                    int nrows) {
+  const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  if (total <= 0) return;
   postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,
-                                                     err);
+                                                     err, rowlist, nrows);
 }
 template <int L>
 void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
@@ -426,7 +432,7 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_preadd<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int,          \
                                  uint32_t*, cudaStream_t);                                              \
   template void launch_postadd<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, uint32_t*, int,   \
-                                  uint32_t*, cudaStream_t);                                             \
+                                  uint32_t*, cudaStream_t, const int*, int);                            \
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);

@@ -56,9 +56,12 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
                    uint32_t* children, int sh, uint32_t* err, cudaStream_t st);
 // Children products (7 per parent, hm x hn) -> parent C (rows x cols, stripped).
 // Optional trace output of Winograd's T1/T2 (2 x hm x hn per parent) when t_out != nullptr.
+// rowlist (device, optional): only these child rows [0, hm) are combined (and the parent rows
+// they produce written) -- the row-owned combine of the multi-GPU path.
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
-                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st);
+                    uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st,
+                    const int* rowlist = nullptr, int nrows = 0);
 
 // copy a (rows x cols) window with leading dims (records) -- used by LU
 template <int L>

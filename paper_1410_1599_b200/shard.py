@@ -10,6 +10,13 @@ each rank.  Elementwise post-additions commute with the split, so the result is
 bit-identical to the single-GPU product (and to the reference).  There is no
 all-reduce: MP rounded sums are not an NCCL reduction and are order-sensitive.
 
+Default combine: instead of gathering every unit product on every rank, one all-to-all
+moves each unit product's row slices to the rank that owns them, and each rank runs
+the post-additions for its rows of C only (mpgpu_fast_combine_rows: ownership
+propagates through the pad/halve index map), so no post-addition is replicated and
+each byte crosses NVLink once.  C stays distributed by rows ('gather' mode keeps the
+all-gather + replicated combine when every rank needs all of C).
+
 Simple / Block (matrix.hpp:178-233): C is split by row blocks (row i of C depends on
 row i of A and all of B; Block's k-tiles are row-independent), then all-gathered.
 
@@ -125,6 +132,151 @@ class _FastSharded:
         return s
 
 
+# ---------------------------------------------------------------------------
+# Row-owned combine: one all-to-all of unit-product row slices, then every rank
+# post-adds only the rows of C it owns (no replicated post-additions).
+# ---------------------------------------------------------------------------
+
+
+def level_rows(m: int, depth: int) -> List[int]:
+    """rows of a level-t node, t = 0 .. depth (pad odd to even, halve)."""
+    out = [m]
+    for _ in range(depth):
+        m = (m + m % 2) // 2
+        out.append(m)
+    return out
+
+
+def owned_c_rows(m: int, depth: int, unit_level: int, lo: int, hi: int) -> List[int]:
+    """Rows of C produced from the unit-level rows [lo, hi): a level-t row r comes from
+    child row r (top quadrants) or r - m_{t+1} (bottom) -- mpgpu_fast_combine_rows."""
+    rows = level_rows(m, depth)
+    owned = [r for r in range(lo, min(hi, rows[unit_level]))]
+    for t in range(unit_level - 1, -1, -1):
+        hm = rows[t + 1]
+        mark = set()
+        for rc in owned:
+            if rc < rows[t]:
+                mark.add(rc)
+            if rc + hm < rows[t]:
+                mark.add(rc + hm)
+        owned = sorted(mark)
+    return owned
+
+
+def a2a_pack_plan(my_units: Shard, rows: List[Shard], um: int, un: int, rw: int):
+    """2D copies (in 32-bit words) of this rank's unit products into the all-to-all send
+    buffer: chunk t holds rows [rows[t].lo, rows[t].hi) of every local unit, padded to
+    my_units.per units x rows[t].per rows.  Returns (copies, chunk words)."""
+    row_w = un * rw
+    unit_w = um * row_w
+    chunk = my_units.per * rows[0].per * row_w
+    nloc = my_units.hi - my_units.lo
+    plan = []
+    for t, rr in enumerate(rows):
+        h = rr.hi - rr.lo
+        if nloc > 0 and h > 0:
+            plan.append(dict(dst=t * chunk, dpitch=rows[0].per * row_w, src=rr.lo * row_w, spitch=unit_w,
+                             width=h * row_w, height=nloc))
+    return plan, chunk
+
+
+def a2a_unpack_plan(units: List[Shard], my_rows: Shard, rows_per: int, um: int, un: int, rw: int):
+    """2D copies from the receive buffer (chunk s = source rank s's units, my rows) into
+    the all-units product buffer (unit-major, only my rows filled)."""
+    row_w = un * rw
+    unit_w = um * row_w
+    chunk = units[0].per * rows_per * row_w
+    h = my_rows.hi - my_rows.lo
+    plan = []
+    for s_, us in enumerate(units):
+        n = us.hi - us.lo
+        if n > 0 and h > 0:
+            plan.append(dict(dst=(us.lo * um + my_rows.lo) * row_w, dpitch=unit_w, src=s_ * chunk,
+                             spitch=rows_per * row_w, width=h * row_w, height=n))
+    return plan
+
+
+def run_plan_torch(plan, dst, src):
+    """Execute a copy plan on flat int32 tensors (CPU or GPU; torch indexing)."""
+    for c in plan:
+        for r in range(c["height"]):
+            d0, s0 = c["dst"] + r * c["dpitch"], c["src"] + r * c["spitch"]
+            dst[d0:d0 + c["width"]] = src[s0:s0 + c["width"]]
+
+
+class _FastRowOwned:
+    """Strassen / Winograd over N GPUs with a row-owned combine: leaf products of the
+    rank's units (mpgpu_fast_leaves), one all_to_all_single of unit-product row slices,
+    then mpgpu_fast_combine_rows for the rank's rows only.  C ends up distributed: rank
+    r holds the rows owned_c_rows(..) of C (the rest of its C buffer is not written)."""
+    replicated = False
+
+    def __init__(self, algo, n_min, da, db, dc, rank, world, group=None):
+        import torch
+        from .mpmm import record_words
+        self.algo, self.n_min, self.da, self.db, self.dc = int(algo), n_min, da, db, dc
+        self.group, self.rank, self.world = group, rank, world
+        m, l, n = da.rows(), da.cols(), db.cols()
+        self.l = l
+        depth, leaves, *_ = fast_plan(m, l, n, n_min)
+        if depth == 0:
+            raise ValueError("leaf sharding needs a recursion (depth >= 1)")
+        self.up = choose_split(depth, world)
+        units = 7 ** (depth - self.up)
+        self.units = even_ranges(units, world)
+        self.shard = self.units[rank]
+        um, un = node_dims(m, l, n, n_min, depth - self.up)
+        self.rows = even_ranges(um, world)
+        self.my_rows = self.rows[rank]
+        rw = record_words(dc.m.nlimbs)
+        self.rw, self.um, self.un = rw, um, un
+        self.pack, chunk = a2a_pack_plan(self.shard, self.rows, um, un, rw)
+        self.unpack = a2a_unpack_plan(self.units, self.my_rows, self.rows[0].per, um, un, rw)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.local = torch.zeros(max(1, self.shard.per * um * un * rw), dtype=torch.int32, device=dev)
+        self.send = torch.zeros(world * chunk, dtype=torch.int32, device=dev)
+        self.recv = torch.zeros_like(self.send)
+        self.full = torch.zeros(units * um * un * rw, dtype=torch.int32, device=dev)
+        self.c_rows = owned_c_rows(m, depth, depth - self.up, self.my_rows.lo, self.my_rows.hi)
+        self.mode = (f"row-owned(up={self.up}, units={units}, per_rank={self.shard.per}, "
+                     f"unit_rows_per_rank={self.rows[0].per})")
+
+    def _copies(self, plan, dst, src):
+        h = self.dc._h
+        for c in plan:
+            _raise_rc(h, _L.lib.mpgpu_copy_device_2d(
+                h, C.c_void_p(dst.data_ptr() + 4 * c["dst"]), 4 * c["dpitch"],
+                C.c_void_p(src.data_ptr() + 4 * c["src"]), 4 * c["spitch"], 4 * c["width"], c["height"]))
+
+    def __call__(self):
+        import torch.distributed as dist
+        from .mpmm import Stats, _raise
+        st = _L.MpgpuStats()
+        h = self.dc._h
+        if self.shard.hi > self.shard.lo:
+            _raise(h, _L.lib.mpgpu_fast_leaves(h, self.algo, self.n_min, C.byref(self.da.m), C.byref(self.db.m),
+                                               self.up, self.shard.lo, self.shard.hi,
+                                               C.c_void_p(self.local.data_ptr()), C.byref(st)))
+        self._copies(self.pack, self.send, self.local)
+        dist.all_to_all_single(self.recv, self.send, group=self.group)
+        self._copies(self.unpack, self.full, self.recv)
+        st2 = _L.MpgpuStats()
+        _raise(h, _L.lib.mpgpu_fast_combine_rows(h, self.algo, self.n_min, self.l, self.up,
+                                                 C.c_void_p(self.full.data_ptr()), self.my_rows.lo,
+                                                 self.my_rows.hi, C.byref(self.dc.m), C.byref(st2)))
+        s = Stats.of(st)
+        s.postadd_ms += st2.postadd_ms
+        s.launches += st2.launches
+        s.mul, s.addsub = _count(self.algo, self.da, self.db, self.n_min)
+        return s
+
+
+def _raise_rc(h, rc):
+    from .mpmm import _raise
+    _raise(h, rc)
+
+
 class _RowSharded:
     replicated = False
     mode = "row-shard"
@@ -177,14 +329,18 @@ def _cuda_copy(h, dst: int, src: int, nbytes: int):
 
 
 def make_runner(algo, param, da, db, dc, rank: int, world: int, mode: str = "auto", group=None):
-    """mode: 'auto' (fast algorithms: leaf shards; simple/block: row shards),
-    'replicas' (independent copies, weak scaling)."""
+    """mode: 'auto' (fast algorithms: leaf shards with the row-owned all-to-all combine;
+    simple/block: row shards), 'gather' (fast algorithms: leaf shards, all-gather of the
+    unit products and a replicated combine -- C complete on every rank), 'replicas'
+    (independent copies, weak scaling)."""
     from .mpmm import Algorithm
     if world <= 1 or mode == "replicas":
         return _Replica(algo, param, da, db, dc)
     if Algorithm(algo) in (Algorithm.strassen, Algorithm.winograd):
         depth, *_ = fast_plan(da.rows(), da.cols(), db.cols(), param)
         if depth >= 1:
-            return _FastSharded(algo, param, da, db, dc, rank, world, group)
+            if mode == "gather":
+                return _FastSharded(algo, param, da, db, dc, rank, world, group)
+            return _FastRowOwned(algo, param, da, db, dc, rank, world, group)
         return _Replica(algo, param, da, db, dc)
     return _RowSharded(algo, param, da, db, dc, rank, world, group)

@@ -76,3 +76,62 @@ def test_gloo_world2_gather_layout(units):
         p.join(120)
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("m,l,n,n_min,up", [(1024, 1024, 1024, 64, 1), (1001, 777, 1537, 32, 1), (45, 37, 51, 5, 0),
+                                            (33, 29, 40, 4, 1), (100, 100, 100, 1, 0)])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_owned_rows_partition_c(m, l, n, n_min, up, world):
+    depth, *_ = shard.fast_plan(m, l, n, n_min)
+    if up >= depth:
+        pytest.skip("split level above the root")
+    um, _ = shard.node_dims(m, l, n, n_min, depth - up)
+    seen = []
+    for rr in shard.even_ranges(um, world):
+        seen += shard.owned_c_rows(m, depth, depth - up, rr.lo, rr.hi)
+    assert sorted(seen) == list(range(m))  # every row of C owned by exactly one rank
+
+
+def _a2a_worker(rank, world, port, units, um, un, rw, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    us = shard.even_ranges(units, world)
+    rows = shard.even_ranges(um, world)
+    me = us[rank]
+    unit_w = um * un * rw
+    local = torch.zeros(max(1, me.per * unit_w), dtype=torch.int32)
+    for u in range(me.lo, me.hi):  # word w of unit u = 100000 u + w
+        local[(u - me.lo) * unit_w:(u - me.lo + 1) * unit_w] = torch.arange(unit_w, dtype=torch.int32) + 100000 * u
+    pack, chunk = shard.a2a_pack_plan(me, rows, um, un, rw)
+    send = torch.zeros(world * chunk, dtype=torch.int32)
+    shard.run_plan_torch(pack, send, local)
+    recv = torch.zeros_like(send)
+    dist.all_to_all_single(recv, send)
+    full = torch.full((units * unit_w,), -1, dtype=torch.int32)
+    shard.run_plan_torch(shard.a2a_unpack_plan(us, rows[rank], rows[0].per, um, un, rw), full, recv)
+    # my rows of every unit hold the owner's words; the rest is untouched
+    ok = True
+    mr = rows[rank]
+    for u in range(units):
+        for r in range(um):
+            seg = full[u * unit_w + r * un * rw:u * unit_w + (r + 1) * un * rw]
+            want = torch.arange(r * un * rw, (r + 1) * un * rw, dtype=torch.int32) + 100000 * u
+            ok &= bool(torch.equal(seg, want)) if mr.lo <= r < mr.hi else bool((seg == -1).all())
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("units,um", [(7, 5), (49, 8), (3, 1)])
+def test_gloo_world2_all_to_all_row_slices(units, um):
+    world, un, rw = 2, 3, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, units, um, un, rw, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}

@@ -62,3 +62,55 @@ def test_row_split_bit_exact(P, algo, param):
         assert L.lib.mpgpu_matrix_view(C.byref(dc.m), r.lo, 0, rows, n, C.byref(cv)) == 0
         assert L.lib.mpgpu_gemm(h, int(P.Algorithm[algo]), param, C.byref(av), C.byref(db.m), C.byref(cv), None) == 0
     assert P.identical(dc.download(), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["strassen", "winograd"])
+@pytest.mark.parametrize("m,l,n,bits,n_min", [(64, 64, 64, 256, 8), (45, 37, 51, 128, 5), (33, 29, 40, 512, 4)])
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("up", [0, 1])
+def test_row_owned_combine_bit_exact(P, algo, m, l, n, bits, n_min, world, up):
+    # every rank's units via mpgpu_fast_leaves, the all-to-all emulated chunk by chunk,
+    # mpgpu_fast_combine_rows per rank; the owned rows of all ranks assemble C exactly
+    ctx = P.PrecisionContext(bits)
+    a, b = P.gen_uniform_full(m, l, 3, ctx), P.gen_uniform_full(l, n, 4, ctx)
+    want = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm[algo], n_min), ctx).c
+    depth, *_ = shard.fast_plan(m, l, n, n_min)
+    if up >= depth:
+        pytest.skip("split level above the root")
+    da, db = a.to_device(), b.to_device()
+    units = 7 ** (depth - up)
+    um, un = shard.node_dims(m, l, n, n_min, depth - up)
+    L_ = P.nlimbs_for(bits)
+    rw = P.record_words(L_)
+    us, rows = shard.even_ranges(units, world), shard.even_ranges(um, world)
+    h = da._h
+    sends = []
+    for r in range(world):
+        local = _rec_tensor(max(1, us[r].per * um * un * rw))
+        if us[r].hi > us[r].lo:
+            assert L.lib.mpgpu_fast_leaves(h, int(P.Algorithm[algo]), n_min, C.byref(da.m), C.byref(db.m), up,
+                                           us[r].lo, us[r].hi, C.c_void_p(local.data_ptr()), None) == 0
+        torch.cuda.synchronize()
+        pack, chunk = shard.a2a_pack_plan(us[r], rows, um, un, rw)
+        send = _rec_tensor(world * chunk)
+        shard.run_plan_torch(pack, send, local)
+        sends.append(send)
+    out = P.Matrix(m, n, ctx)
+    covered = []
+    for r in range(world):
+        recv = torch.cat([sends[s].narrow(0, r * chunk, chunk) for s in range(world)])
+        full = _rec_tensor(units * um * un * rw)
+        shard.run_plan_torch(shard.a2a_unpack_plan(us, rows[r], rows[0].per, um, un, rw), full, recv)
+        dc = P.DeviceMatrix(m, n, ctx)
+        assert L.lib.mpgpu_fast_combine_rows(h, int(P.Algorithm[algo]), n_min, l, up, C.c_void_p(full.data_ptr()),
+                                             rows[r].lo, rows[r].hi, C.byref(dc.m), None) == 0
+        part = dc.download()
+        own = shard.owned_c_rows(m, depth, depth - up, rows[r].lo, rows[r].hi)
+        covered += own
+        idx = (np.asarray(own, dtype=np.int64)[:, None] * n + np.arange(n)[None, :]).reshape(-1)
+        out.limbs[:, idx] = part.limbs[:, idx]
+        out.exp[idx] = part.exp[idx]
+        out.sign[idx] = part.sign[idx]
+    assert sorted(covered) == list(range(m))
+    assert P.identical(out, want)

@@ -204,11 +204,12 @@ __device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t s
 // ---------------------------------------------------------------------------
 // z = RN_p(x * y)   (mpfr_mul, precision.hpp:145-151; matrix.hpp:150,152)
 // ---------------------------------------------------------------------------
-template <int L, class AG>
+// NZ: the caller guarantees both operands are nonzero (no zero test)
+template <int L, class AG, bool NZ = false>
 __device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const MP<L>& y, int sh,
                                          MP<L>& z) {
   z.s = xs ^ y.s;
-  if (xe == EXP_ZERO || y.e == EXP_ZERO) {
+  if (!NZ && (xe == EXP_ZERO || y.e == EXP_ZERO)) {
 #pragma unroll
     for (int k = 0; k < L; ++k) z.m[k] = 0;
     z.e = EXP_ZERO;
@@ -267,12 +268,13 @@ __device__ __forceinline__ void mp_mul(const MP<L>& x, const MP<L>& y, int sh, M
 // Exact-alignment algorithm over an (L+1)-limb window (one guard limb) plus a
 // sticky bit; see DESIGN.md "MP add".  Exact cancellation gives +0 (RNDN).
 // ---------------------------------------------------------------------------
-template <int L>
+// NZ: the caller guarantees both operands are nonzero (no zero test)
+template <int L, bool NZ = false>
 __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32_t negy, int sh,
                                        MP<L>& z) {
   // z may alias x or y: every input is read before z is written.
   const uint32_t ys = y_in.s ^ negy;
-  if (x.e == EXP_ZERO || y_in.e == EXP_ZERO) {
+  if (!NZ && (x.e == EXP_ZERO || y_in.e == EXP_ZERO)) {
     if (x.e == EXP_ZERO && y_in.e == EXP_ZERO) {
       const uint32_t zs = x.s & ys;  // (-0) + (-0) = -0, otherwise +0 under RNDN
 #pragma unroll

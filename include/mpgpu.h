@@ -44,11 +44,11 @@ extern "C" {
 #define MPGPU_ERR_UNDEFINED_METRIC 6 /* mpmm::UndefinedMetricError (errors.hpp:41-43) */
 
 #define MPGPU_EXP_ZERO INT32_MIN
-#define MPGPU_MAX_PREC 1024 /* largest precision of the arithmetic entry points (32 limbs) */
-/* Matrices may be allocated, uploaded and downloaded up to MPGPU_MAX_STORE_PREC (64
- * limbs) -- the double-precision references of the accuracy metrics; every other
- * entry point rejects them with DOMAIN. */
-#define MPGPU_MAX_STORE_PREC 2048
+/* Largest device precision: limb counts 1, 2, 4, 8, 16, 32 (register-resident, <= 1024
+ * bits) and 64, 128, 256, 288 (wide formats in local memory, <= 9216 bits -- e.g. the
+ * 8192 / 8650-bit Lotkin experiments of the paper). */
+#define MPGPU_MAX_PREC 9216
+#define MPGPU_MAX_STORE_PREC MPGPU_MAX_PREC
 
 /* mpmm::Algorithm (fastmm.hpp:13) */
 enum { MPGPU_SIMPLE = 0, MPGPU_BLOCK = 1, MPGPU_STRASSEN = 2, MPGPU_WINOGRAD = 3 };

@@ -18,7 +18,8 @@ BUILD = PKG / "_build"
 LIB = PKG / "libmpgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu"]
+SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu",
+           "gemm_wide.cu", "metrics_wide.cu", "elementwise_wide.cu", "lu_wide.cu"]
 HEADERS = ["mp_arith.cuh", "kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -33,7 +34,8 @@ def _newest_dep() -> float:
 def _compile(src: str, force: bool) -> Path:
     obj = BUILD / (src + ".o")
     s = CSRC / src
-    if (not force and obj.exists() and obj.stat().st_mtime >= s.stat().st_mtime
+    srcs = [s] + ([CSRC / src.replace("_wide", "")] if "_wide" in src else [])  # *_wide.cu include *.cu
+    if (not force and obj.exists() and all(obj.stat().st_mtime >= x.stat().st_mtime for x in srcs)
             and obj.stat().st_mtime >= _newest_dep()):
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(obj)]

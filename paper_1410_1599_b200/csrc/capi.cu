@@ -55,7 +55,7 @@ int fail(mpgpu_handle* h, int code, const char* fmt, ...) {
                   "%s: %s", #expr, cudaGetErrorString(e_));                                 \
   } while (0)
 
-constexpr int kLimbOptions[] = {1, 2, 4, 8, 16, 32, 64};  // 64: storage / metrics only
+constexpr int kLimbOptions[] = {1, 2, 4, 8, 16, 32, 64, 128, 256, 288};  // > 32: *_wide.cu
 
 int nlimbs_for(int32_t prec) {
   if (prec < 2 || prec > MPGPU_MAX_STORE_PREC) return 0;
@@ -74,14 +74,16 @@ int dispatch_L(int L, F&& f) {
     case 8: return f(std::integral_constant<int, 8>{});
     case 16: return f(std::integral_constant<int, 16>{});
     case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    case 288: return f(std::integral_constant<int, 288>{});
     default: return MPGPU_ERR_DOMAIN;
   }
 }
 
-// storage-level dispatch (record conversion, accuracy metrics): also 64 limbs
 template <class F>
 int dispatch_store(int L, F&& f) {
-  if (L == 64) return f(std::integral_constant<int, 64>{});
   return dispatch_L(L, std::forward<F>(f));
 }
 
@@ -617,12 +619,11 @@ int run_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* l
   return MPGPU_OK;
 }
 
-// arithmetic entry points: 64-limb (p > 1024) matrices are storage / metrics only
+// arithmetic entry points: every supported limb count has kernels
 int compute_range(mpgpu_handle* h, std::initializer_list<const mpgpu_mat*> ms) {
   for (const mpgpu_mat* m : ms)
-    if (m && m->nlimbs > 32)
-      return fail(h, MPGPU_ERR_DOMAIN, "precision %d above %d bits: storage and accuracy metrics only", m->prec,
-                  MPGPU_MAX_PREC);
+    if (m && m->prec > MPGPU_MAX_PREC)
+      return fail(h, MPGPU_ERR_DOMAIN, "precision %d above %d bits", m->prec, MPGPU_MAX_PREC);
   return MPGPU_OK;
 }
 
@@ -925,8 +926,7 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
   // and B, the product, conversion + D2H of C, and a single synchronisation.
   if (!h) return MPGPU_ERR_DOMAIN;
   const int L = nlimbs_for(prec);
-  if (!L || L > 32)
-    return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
+  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
   if (m < 1 || l < 1 || n < 1) return fail(h, MPGPU_ERR_DIMENSION, "matrix dimensions must be at least 1x1");
   if (Lh < (prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
   mpgpu_mat A{m, l, prec, L, nullptr, l, 0}, B{l, n, prec, L, nullptr, n, 0}, C{m, n, prec, L, nullptr, n, 0};
@@ -1504,7 +1504,7 @@ int mpgpu_recursion_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t
 
 int mpgpu_gen(int kind, int64_t N, uint64_t seed, int32_t prec, uint32_t* limbs, int32_t* exp, uint8_t* sign,
               int32_t Lh) {
-  if (prec < 2 || prec > MPGPU_MAX_STORE_PREC || Lh < (prec + 31) / 32) return MPGPU_ERR_DOMAIN;
+  if (prec < 2 || prec > MPGPU_MAX_PREC || Lh < (prec + 31) / 32) return MPGPU_ERR_DOMAIN;
   Prng64 rng(seed);
   for (int64_t e = 0; e < N; ++e) {
     if (kind == 0) {

@@ -436,15 +436,18 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);
-// 64 limbs (p <= 2048): storage only -- references of the accuracy metrics (metrics.cu)
-template void launch_soa2rec<64>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t, uint32_t*,
-                                 cudaStream_t);
-template void launch_rec2soa<64>(const uint32_t*, int64_t, uint32_t*, int32_t*, uint8_t*, int64_t, cudaStream_t);
+#if MPG_WIDE
+MPG_INST(64)
+MPG_INST(128)
+MPG_INST(256)
+MPG_INST(288)
+#else
 MPG_INST(1)
 MPG_INST(2)
 MPG_INST(4)
 MPG_INST(8)
 MPG_INST(16)
 MPG_INST(32)
+#endif
 
 }  // namespace mpg

@@ -76,7 +76,10 @@ __device__ __forceinline__ void cp_async_wait() {
 // outputs of one row (columns tx, tx+TN, ...) -- U independent accumulation chains
 // per thread share the a-record
 template <int L>
-struct GemmCfg;
+struct GemmCfg {  // wide formats (L = 64 .. 288, gemm_wide.cu): mantissas in local memory
+  static constexpr int MINB = 1, TM = 8, TN = 16, TK = 2, U = 1;
+  static constexpr int KU = 1;
+};
 template <>
 struct GemmCfg<1> {
   static constexpr int MINB = MPG_MINB_1, TM = 16, TN = 16, TK = 16, U = 1;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 
 template <int L>
 void launch_gemm(const GemmArgs& g, cudaStream_t st) {
-  if constexpr (L >= 8) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
+  if constexpr (L == 8 || L == 16 || L == 32) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
     if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
   }
   constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
@@ -269,11 +272,18 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
   }
 }
 
+#if MPG_WIDE
+template void launch_gemm<64>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<128>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<256>(const GemmArgs&, cudaStream_t);
+template void launch_gemm<288>(const GemmArgs&, cudaStream_t);
+#else
 template void launch_gemm<1>(const GemmArgs&, cudaStream_t);
 template void launch_gemm<2>(const GemmArgs&, cudaStream_t);
 template void launch_gemm<4>(const GemmArgs&, cudaStream_t);
 template void launch_gemm<8>(const GemmArgs&, cudaStream_t);
 template void launch_gemm<16>(const GemmArgs&, cudaStream_t);
 template void launch_gemm<32>(const GemmArgs&, cudaStream_t);
+#endif
 
 }  // namespace mpg

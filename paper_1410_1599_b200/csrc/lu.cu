@@ -650,11 +650,18 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
                                        uint64_t*, int64_t*, int, cudaStream_t);                                      \
   template void launch_lu_solve<L>(const uint32_t*, int64_t, const int64_t*, const uint32_t*, uint32_t*,        \
                                    uint32_t*, int, uint32_t*, int64_t*, int, int64_t, cudaStream_t);
+#if MPG_WIDE
+MPG_LU_INST(64)
+MPG_LU_INST(128)
+MPG_LU_INST(256)
+MPG_LU_INST(288)
+#else
 MPG_LU_INST(1)
 MPG_LU_INST(2)
 MPG_LU_INST(4)
 MPG_LU_INST(8)
 MPG_LU_INST(16)
 MPG_LU_INST(32)
+#endif
 
 }  // namespace mpg

@@ -203,12 +203,18 @@ void launch_reduce3(const uint32_t* A, const uint32_t* B, int64_t N, uint32_t* o
                                     uint32_t*, uint32_t*, unsigned long long*, uint32_t*, cudaStream_t);        \
   template void launch_colsum_abs<L>(const uint32_t*, int64_t, int, int, int, uint32_t*, uint32_t*, cudaStream_t); \
   template void launch_reduce3<L>(const uint32_t*, const uint32_t*, int64_t, uint32_t*, uint32_t*, cudaStream_t);
+#if MPG_WIDE
+MPG_METRICS_INST(64)
+MPG_METRICS_INST(128)
+MPG_METRICS_INST(256)
+MPG_METRICS_INST(288)
+#else
 MPG_METRICS_INST(1)
 MPG_METRICS_INST(2)
 MPG_METRICS_INST(4)
 MPG_METRICS_INST(8)
 MPG_METRICS_INST(16)
 MPG_METRICS_INST(32)
-MPG_METRICS_INST(64)
+#endif
 
 }  // namespace mpg

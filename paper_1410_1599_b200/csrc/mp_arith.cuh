@@ -12,6 +12,15 @@
 #pragma once
 #include <cstdint>
 
+// Limb loops: fully unrolled for the register-resident formats (L <= 32).  The wide
+// formats (L = 64 .. 288, up to 9216 bits) are compiled in separate translation units
+// (*_wide.cu, MPG_WIDE=1) where the same code runs as loops over local-memory arrays.
+#if MPG_WIDE
+#define MPG_UNROLL _Pragma("unroll 1")
+#else
+#define MPG_UNROLL _Pragma("unroll")
+#endif
+
 namespace mpg {
 
 constexpr int32_t EXP_ZERO = INT32_MIN;
@@ -47,13 +56,13 @@ struct MP {
 // plus ~1.3 ALU carry ops per limb product -- no half-rate IMAD.HI.
 template <int L, class AG>
 __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < 2 * L; ++i) r[i] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < L; ++i) {
     const uint32_t ai = a_at(i);
     uint32_t carry = 0;
-#pragma unroll
+MPG_UNROLL
     for (int j = 0; j < L; ++j) {
       const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
       r[i + j] = (uint32_t)t;
@@ -65,9 +74,9 @@ __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint
 #else
 template <int L, class AG>
 __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < 2 * L; ++i) r[i] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < L; ++i) {
     const uint32_t ai = a_at(i);
     if (L == 1) {
@@ -75,12 +84,12 @@ __device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint
       asm("mul.hi.u32 %0, %1, %2;" : "=r"(r[1]) : "r"(ai), "r"(b[0]));
     } else {
       asm volatile("mad.lo.cc.u32 %0, %1, %2, %0;" : "+r"(r[i]) : "r"(ai), "r"(b[0]));
-#pragma unroll
+MPG_UNROLL
       for (int j = 1; j < L; ++j)
         asm volatile("madc.lo.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + j]) : "r"(ai), "r"(b[j]));
       asm volatile("addc.u32 %0, %0, 0;" : "+r"(r[i + L]));
       asm volatile("mad.hi.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + 1]) : "r"(ai), "r"(b[0]));
-#pragma unroll
+MPG_UNROLL
       for (int j = 1; j < L; ++j)
         asm volatile("madc.hi.cc.u32 %0, %1, %2, %0;" : "+r"(r[i + j + 1]) : "r"(ai), "r"(b[j]));
       if (i + L + 1 < 2 * L) asm volatile("addc.u32 %0, %0, 0;" : "+r"(r[i + L + 1]));
@@ -102,14 +111,14 @@ __device__ __forceinline__ void mul_full(const uint32_t (&a)[L], const uint32_t 
 // products instead of L^2 -- the mulhigh trick MPFR itself uses for mpfr_mul.
 template <int L, class AG>
 __device__ __forceinline__ void mul_high_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < 2 * L; ++i) r[i] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int i = 0; i < L; ++i) {
     const uint32_t ai = a_at(i);
     const int j0 = (L - 2 - i) > 0 ? (L - 2 - i) : 0;
     uint32_t carry = 0;
-#pragma unroll
+MPG_UNROLL
     for (int j = j0; j < L; ++j) {
       const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
       r[i + j] = (uint32_t)t;
@@ -122,6 +131,15 @@ __device__ __forceinline__ void mul_high_g(AG a_at, const uint32_t (&b)[L], uint
 // add a single word w at limb 0 with full carry propagation; returns carry-out
 template <int L>
 __device__ __forceinline__ uint32_t add_word(uint32_t (&m)[L], uint32_t w) {
+  if constexpr (L > 32) {  // wide formats: plain 64-bit carries (no PTX carry chains in loops)
+    uint64_t c = w;
+    for (int k = 0; k < L && c; ++k) {
+      const uint64_t t = (uint64_t)m[k] + c;
+      m[k] = (uint32_t)t;
+      c = t >> 32;
+    }
+    return (uint32_t)c;
+  }
   uint32_t c;
   if (L == 1) {
     asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(m[0]) : "r"(w));
@@ -129,7 +147,7 @@ __device__ __forceinline__ uint32_t add_word(uint32_t (&m)[L], uint32_t w) {
     return c;
   }
   asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(m[0]) : "r"(w));
-#pragma unroll
+MPG_UNROLL
   for (int k = 1; k < L; ++k) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(m[k]));
   asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
   return c;
@@ -162,7 +180,7 @@ __device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t s
     const int rbpos = sh - 1, rl = rbpos >> 5, rbit = rbpos & 31;
     const int ql = sh >> 5, qb = sh & 31;
     uint32_t stk = g | st, rb = 0, lsb = 0;
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L; ++k) {
       uint32_t v = m[k];
       if (k < rl) {
@@ -178,7 +196,7 @@ __device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t s
     }
     const uint32_t up = rb & ((stk != 0) | lsb);
     uint32_t c = 0;
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L; ++k) {
       const uint32_t addend = (k == ql) ? (up << qb) : 0u;
       const uint64_t t = (uint64_t)m[k] + addend + c;
@@ -186,7 +204,7 @@ __device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t s
       c = (uint32_t)(t >> 32);
     }
     if (c) {
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < L - 1; ++k) m[k] = 0;
       m[L - 1] = 0x80000000u;
       e += 1;
@@ -194,7 +212,7 @@ __device__ __forceinline__ void round_p(uint32_t (&m)[L], uint32_t g, uint32_t s
     return;
   }
   if (add_word<L>(m, up_word)) {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L - 1; ++k) m[k] = 0;
     m[L - 1] = 0x80000000u;
     e += 1;
@@ -210,7 +228,7 @@ __device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const
                                          MP<L>& z) {
   z.s = xs ^ y.s;
   if (!NZ && (xe == EXP_ZERO || y.e == EXP_ZERO)) {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L; ++k) z.m[k] = 0;
     z.e = EXP_ZERO;
     return;
@@ -225,11 +243,11 @@ __device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const
     const bool down = gt < 0x80000000u - 2u * L;
     const bool up = gt > 0x80000000u && gt < 0xFFFFFFFFu - 2u * L;
     if (down | up) {
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], t1);
       int32_t e = xe + y.e - (int32_t)t1;
       if (add_word<L>(z.m, up ? 1u : 0u)) {
-#pragma unroll
+MPG_UNROLL
         for (int k = 0; k < L - 1; ++k) z.m[k] = 0;
         z.m[L - 1] = 0x80000000u;
         e += 1;
@@ -242,12 +260,12 @@ __device__ __forceinline__ void mp_mul_g(AG a_at, int32_t xe, uint32_t xs, const
   // normalise branch-free: shift left by one when the product's top bit is clear
   const uint32_t s1 = (P[2 * L - 1] >> 31) ^ 1u;
   const int32_t e = xe + y.e - (int32_t)s1;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], s1);
   uint32_t g, st = 0;
   if (L >= 2) {
     g = __funnelshift_l(P[L >= 2 ? L - 2 : 0], P[L - 1], s1);
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L - 2; ++k) st |= P[k];
     st |= P[L >= 2 ? L - 2 : 0] << s1;
   } else {
@@ -277,12 +295,12 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
   if (!NZ && (x.e == EXP_ZERO || y_in.e == EXP_ZERO)) {
     if (x.e == EXP_ZERO && y_in.e == EXP_ZERO) {
       const uint32_t zs = x.s & ys;  // (-0) + (-0) = -0, otherwise +0 under RNDN
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < L; ++k) z.m[k] = 0;
       z.e = EXP_ZERO;
       z.s = zs;
     } else if (x.e == EXP_ZERO) {
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < L; ++k) z.m[k] = y_in.m[k];
       z.e = y_in.e;
       z.s = ys;
@@ -296,7 +314,7 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
   uint32_t A[W], B[W];
   A[0] = 0;
   B[0] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) {
     A[k + 1] = swp ? y_in.m[k] : x.m[k];
     B[k + 1] = swp ? x.m[k] : y_in.m[k];
@@ -313,26 +331,26 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
   if (d >= 32u) {
     if (d >= 32u * W) {
       st = 1;
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < W; ++k) B[k] = 0;
     } else {
       uint32_t q = d >> 5;
       const uint32_t r = d & 31u;
       while (q) {
         st |= B[0];
-#pragma unroll
+MPG_UNROLL
         for (int k = 0; k < W - 1; ++k) B[k] = B[k + 1];
         B[W - 1] = 0;
         --q;
       }
       st |= B[0] & ((1u << r) - 1u);
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], r);
       B[W - 1] >>= r;
       st = st != 0;
     }
   } else {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], d);
     B[W - 1] >>= d;
   }
@@ -341,31 +359,53 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
   const uint32_t mask = 0u - sub;
   const uint32_t cin = sub & (st ^ 1u);
   uint32_t R[W], cout;
-  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(B[0] ^ mask), "r"(cin));  // A[0] == 0
-#pragma unroll
-  for (int k = 1; k < W; ++k) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k] ^ mask));
-  asm volatile("addc.u32 %0, 0, 0;" : "=r"(cout));
+  if constexpr (L > 32) {
+    uint64_t c = (uint64_t)(B[0] ^ mask) + cin;  // A[0] == 0
+    R[0] = (uint32_t)c;
+    c >>= 32;
+    for (int k = 1; k < W; ++k) {
+      c += (uint64_t)A[k] + (B[k] ^ mask);
+      R[k] = (uint32_t)c;
+      c >>= 32;
+    }
+    cout = (uint32_t)c;
+  } else {
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(B[0] ^ mask), "r"(cin));  // A[0] == 0
+MPG_UNROLL
+    for (int k = 1; k < W; ++k)
+      asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k] ^ mask));
+    asm volatile("addc.u32 %0, 0, 0;" : "=r"(cout));
+  }
   int32_t e = ebig;
   uint32_t s = sbig;
   if (sub & ((cout ^ 1u) | (R[W - 1] == 0))) {  // rare: |small| > |big| (d == 0) or deep cancellation
     if (!cout) {
-      asm volatile("sub.cc.u32 %0, 0, %0;" : "+r"(R[0]));
-#pragma unroll
-      for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, 0, %0;" : "+r"(R[k]));
+      if constexpr (L > 32) {  // R = -R
+        uint64_t bo = 0;
+        for (int k = 0; k < W; ++k) {
+          const uint64_t d = 0ull - R[k] - bo;
+          R[k] = (uint32_t)d;
+          bo = (d >> 32) & 1u;
+        }
+      } else {
+        asm volatile("sub.cc.u32 %0, 0, %0;" : "+r"(R[0]));
+MPG_UNROLL
+        for (int k = 1; k < W; ++k) asm volatile("subc.cc.u32 %0, 0, %0;" : "+r"(R[k]));
+      }
       s = ssmall;
     }
     uint32_t any = 0;
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < W; ++k) any |= R[k];
     if (!any) {  // exact cancellation: +0 under RNDN
-#pragma unroll
+MPG_UNROLL
       for (int k = 0; k < L; ++k) z.m[k] = 0;
       z.e = EXP_ZERO;
       z.s = 0;
       return;
     }
     while (R[W - 1] == 0) {
-#pragma unroll
+MPG_UNROLL
       for (int k = W - 1; k > 0; --k) R[k] = R[k - 1];
       R[0] = 0;
       e -= 32;
@@ -374,15 +414,15 @@ __device__ __forceinline__ void mp_add(const MP<L>& x, const MP<L>& y_in, uint32
   // ---- normalise branch-free: add overflow shifts right by one, cancellation left by lz
   const uint32_t c1 = cout & (sub ^ 1u);
   st |= R[0] & c1;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < W - 1; ++k) R[k] = __funnelshift_r(R[k], R[k + 1], c1);
   R[W - 1] = (R[W - 1] >> c1) | (c1 << 31);
   const uint32_t lz = __clz(R[W - 1]);
-#pragma unroll
+MPG_UNROLL
   for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], lz);
   R[0] <<= lz;
   e += (int32_t)c1 - (int32_t)lz;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) z.m[k] = R[k + 1];
   round_p<L>(z.m, R[0], st, sh, e);
   z.e = e;
@@ -398,7 +438,7 @@ template <int L>
 __device__ __forceinline__ void mp_div_bits(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
   z.s = x.s ^ y.s;
   if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L; ++k) z.m[k] = 0;
     z.e = EXP_ZERO;
     return;
@@ -407,20 +447,20 @@ __device__ __forceinline__ void mp_div_bits(const MP<L>& x, const MP<L>& y, int 
   const int p = 32 * L - sh;
   const int nl = (p + 2 + 31) >> 5;  // quotient limbs to produce (<= W)
   uint32_t R[W], Q[W];
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) R[k] = x.m[k];
   R[L] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < W; ++k) Q[k] = 0;
   bool first_bit = true;
-#pragma unroll
+MPG_UNROLL
   for (int ql = W - 1; ql >= 0; --ql) {
     if (W - 1 - ql < nl) {
       uint32_t word = 0;
 #pragma unroll 1
       for (int b = 0; b < 32; ++b) {
         if (!first_bit) {  // R <<= 1
-#pragma unroll
+MPG_UNROLL
           for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], 1);
           R[0] <<= 1;
         }
@@ -428,12 +468,12 @@ __device__ __forceinline__ void mp_div_bits(const MP<L>& x, const MP<L>& y, int 
         // T = R - Y (Y has a zero top limb)
         uint32_t T[W], bo;
         asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(R[0]), "r"(y.m[0]));
-#pragma unroll
+MPG_UNROLL
         for (int k = 1; k < L; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(T[k]) : "r"(R[k]), "r"(y.m[k]));
         asm volatile("subc.cc.u32 %0, %1, 0;" : "=r"(T[L]) : "r"(R[L]));
         asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
         const uint32_t qb = bo ? 0u : 1u;
-#pragma unroll
+MPG_UNROLL
         for (int k = 0; k < W; ++k) R[k] = qb ? T[k] : R[k];
         word = (word << 1) | qb;
       }
@@ -441,17 +481,17 @@ __device__ __forceinline__ void mp_div_bits(const MP<L>& x, const MP<L>& y, int 
     }
   }
   uint32_t rem = 0;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < W; ++k) rem |= R[k];
   int32_t e = x.e - y.e;
   if (Q[W - 1] >> 31) {
     e += 1;
   } else {
-#pragma unroll
+MPG_UNROLL
     for (int k = W - 1; k > 0; --k) Q[k] = __funnelshift_l(Q[k - 1], Q[k], 1);
     Q[0] <<= 1;
   }
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) z.m[k] = Q[k + 1];
   round_p<L>(z.m, Q[0], rem, sh, e);
   z.e = e;
@@ -468,26 +508,37 @@ template <int L>
 __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, MP<L>& z) {
   z.s = x.s ^ y.s;
   if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < L; ++k) z.m[k] = 0;
     z.e = EXP_ZERO;
     return;
   }
   constexpr int W = L + 1;
   uint32_t R[W];
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) R[k] = x.m[k];
   R[L] = 0;
   // R -= Y if R >= Y; returns 1 if subtracted
   auto try_sub = [&]() -> uint32_t {
     uint32_t T[W], bo;
-    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(R[0]), "r"(y.m[0]));
-#pragma unroll
-    for (int k = 1; k < L; ++k) asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(T[k]) : "r"(R[k]), "r"(y.m[k]));
-    asm volatile("subc.cc.u32 %0, %1, 0;" : "=r"(T[L]) : "r"(R[L]));
-    asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
+    if constexpr (L > 32) {
+      uint64_t b = 0;
+      for (int k = 0; k < W; ++k) {
+        const uint64_t d = (uint64_t)R[k] - (k < L ? y.m[k < L ? k : 0] : 0u) - b;
+        T[k] = (uint32_t)d;
+        b = (d >> 32) & 1u;
+      }
+      bo = (uint32_t)b;
+    } else {
+      asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(R[0]), "r"(y.m[0]));
+MPG_UNROLL
+      for (int k = 1; k < L; ++k)
+        asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(T[k]) : "r"(R[k]), "r"(y.m[k]));
+      asm volatile("subc.cc.u32 %0, %1, 0;" : "=r"(T[L]) : "r"(R[L]));
+      asm volatile("subc.u32 %0, 0, 0;" : "=r"(bo));
+    }
     const uint32_t ok = bo ? 0u : 1u;
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < W; ++k) R[k] = ok ? T[k] : R[k];
     return ok;
   };
@@ -501,7 +552,7 @@ __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, M
 #pragma unroll 1
   for (int t = W - 1; t >= 0; --t) {
     // R <<= 32 (R < Y, so the top limb is free)
-#pragma unroll
+MPG_UNROLL
     for (int k = W - 1; k > 0; --k) R[k] = R[k - 1];
     R[0] = 0;
     // estimate q = floor(R / Y) from the top three limbs of R, rounded down
@@ -512,7 +563,7 @@ __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, M
     uint32_t qh = qd >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)qd;
     // R -= qh * Y (exact, W limbs); qh <= q so no underflow
     uint32_t c = 0, b = 0;
-#pragma unroll
+MPG_UNROLL
     for (int j = 0; j < L; ++j) {
       const uint64_t pr = (uint64_t)qh * y.m[j] + c;
       c = (uint32_t)(pr >> 32);
@@ -526,21 +577,21 @@ __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, M
     Q[t] = qh;
   }
   uint32_t rem = 0;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < W; ++k) rem |= R[k];
   // normalise: value = Q[W] . Q[W-1] Q[W-2] ... (radix 2^32)
   int32_t e = x.e - y.e;
   uint32_t M[W];
   if (Q[W]) {  // quotient in [1, 2): shift the digit string right by one bit
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < W; ++k) M[k] = __funnelshift_r(Q[k], Q[k + 1], 1);
     rem |= Q[0] & 1u;
     e += 1;
   } else {
-#pragma unroll
+MPG_UNROLL
     for (int k = 0; k < W; ++k) M[k] = Q[k];
   }
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) z.m[k] = M[k + 1];
   round_p<L>(z.m, M[0], rem, sh, e);
   z.e = e;
@@ -548,7 +599,7 @@ __device__ __forceinline__ void mp_div(const MP<L>& x, const MP<L>& y, int sh, M
 
 template <int L>
 __device__ __forceinline__ void mp_zero(MP<L>& z, uint32_t s = 0) {
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) z.m[k] = 0;
   z.e = EXP_ZERO;
   z.s = s;
@@ -560,7 +611,7 @@ __device__ __forceinline__ int mp_cmpabs(const MP<L>& x, const MP<L>& y) {
   const bool xz = x.e == EXP_ZERO, yz = y.e == EXP_ZERO;
   if (xz || yz) return xz ? (yz ? 0 : -1) : 1;
   if (x.e != y.e) return x.e > y.e ? 1 : -1;
-#pragma unroll
+MPG_UNROLL
   for (int k = L - 1; k >= 0; --k)
     if (x.m[k] != y.m[k]) return x.m[k] > y.m[k] ? 1 : -1;
   return 0;
@@ -578,7 +629,7 @@ __device__ __forceinline__ void load_rec(const uint32_t* __restrict__ r, MP<L>& 
   constexpr int S = rec_stride(L);
   static_assert(S % 4 == 0, "record stride must be a multiple of 4 words");
   uint32_t w[S];
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < S; k += 4) {
     const uint4 v = *reinterpret_cast<const uint4*>(r + k);
     w[k] = v.x;
@@ -586,7 +637,7 @@ __device__ __forceinline__ void load_rec(const uint32_t* __restrict__ r, MP<L>& 
     w[k + 2] = v.z;
     w[k + 3] = v.w;
   }
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) x.m[k] = w[k];
   x.e = (int32_t)w[L];
   x.s = w[L + 1];
@@ -596,7 +647,7 @@ __device__ __forceinline__ void load_rec(const uint32_t* __restrict__ r, MP<L>& 
 // lets the register allocator keep loop-carried accumulators in place
 template <int L>
 __device__ __forceinline__ void load_rec_s(const uint32_t* __restrict__ r, MP<L>& x) {
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) x.m[k] = r[k];
   x.e = (int32_t)r[L];
   x.s = r[L + 1];
@@ -606,13 +657,13 @@ template <int L>
 __device__ __forceinline__ void store_rec(uint32_t* __restrict__ r, const MP<L>& x) {
   constexpr int S = rec_stride(L);
   uint32_t w[S];
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < L; ++k) w[k] = x.m[k];
   w[L] = (uint32_t)x.e;
   w[L + 1] = x.s;
-#pragma unroll
+MPG_UNROLL
   for (int k = L + 2; k < S; ++k) w[k] = 0;
-#pragma unroll
+MPG_UNROLL
   for (int k = 0; k < S; k += 4)
     *reinterpret_cast<uint4*>(r + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
 }

@@ -121,7 +121,9 @@ class _FastSharded:
             _raise(h, _L.lib.mpgpu_fast_leaves(h, self.algo, self.n_min, C.byref(self.da.m), C.byref(self.db.m),
                                                self.up, self.shard.lo, self.shard.hi,
                                                C.c_void_p(self.local.data_ptr()), C.byref(st)))
+        _streams_join(h)
         dist.all_gather_into_tensor(self.all, self.local, group=self.group)
+        _streams_join(h)
         st2 = _L.MpgpuStats()
         _raise(h, _L.lib.mpgpu_fast_combine(h, self.algo, self.n_min, self.l, self.up,
                                             C.c_void_p(self.all.data_ptr()), C.byref(self.dc.m), C.byref(st2)))
@@ -259,7 +261,9 @@ class _FastRowOwned:
                                                self.up, self.shard.lo, self.shard.hi,
                                                C.c_void_p(self.local.data_ptr()), C.byref(st)))
         self._copies(self.pack, self.send, self.local)
+        _streams_join(h)
         dist.all_to_all_single(self.recv, self.send, group=self.group)
+        _streams_join(h)
         self._copies(self.unpack, self.full, self.recv)
         st2 = _L.MpgpuStats()
         _raise(h, _L.lib.mpgpu_fast_combine_rows(h, self.algo, self.n_min, self.l, self.up,
@@ -270,6 +274,17 @@ class _FastRowOwned:
         s.launches += st2.launches
         s.mul, s.addsub = _count(self.algo, self.da, self.db, self.n_min)
         return s
+
+
+def _streams_join(h):
+    """Order the library's stream and torch's current stream (where NCCL collectives are
+    enqueued): a no-op when the handle already runs on torch's stream (bench.py sets it)."""
+    import torch
+    cur = torch.cuda.current_stream()
+    if _L.lib.mpgpu_get_stream(h) == cur.cuda_stream:
+        return
+    _L.lib.mpgpu_synchronize(h)
+    cur.synchronize()
 
 
 def _raise_rc(h, rc):
@@ -308,7 +323,9 @@ class _RowSharded:
             cv.rec, cv.ld, cv.owned = self.local.data_ptr(), self.db.cols(), 0
             _raise(h, _L.lib.mpgpu_gemm(h, self.algo, self.param, C.byref(av), C.byref(self.db.m), C.byref(cv),
                                         C.byref(st)))
+        _streams_join(h)
         dist.all_gather_into_tensor(self.all, self.local.clone(), group=self.group)
+        _streams_join(h)
         # assemble C (rows beyond m are padding)
         nbytes = self.dc.rows() * self.words_per_row * 4
         _cuda_copy(h, self.dc.data_ptr, self.all.data_ptr(), nbytes)

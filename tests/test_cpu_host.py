@@ -113,6 +113,7 @@ def test_pad_even_and_equal_values(P):
 
 
 def test_mpgpu_nlimbs(P):
-    # 1025..2048 bits: 64 limbs, storage / accuracy metrics only (mpgpu.h MPGPU_MAX_STORE_PREC)
-    assert [P.nlimbs_for(b) for b in (1, 2, 32, 33, 64, 65, 128, 129, 256, 512, 1024, 1025, 2048, 2049)] == \
-        [0, 1, 1, 2, 2, 4, 4, 8, 8, 16, 32, 64, 64, 0]
+    # wide formats above 1024 bits: 64, 128, 256, 288 limbs (mpgpu.h MPGPU_MAX_PREC = 9216)
+    assert [P.nlimbs_for(b) for b in (1, 2, 32, 33, 64, 65, 128, 129, 256, 512, 1024, 1025, 2048, 2049, 8192,
+                                      8650, 9216, 9217)] == \
+        [0, 1, 1, 2, 2, 4, 4, 8, 8, 16, 32, 64, 64, 128, 256, 288, 288, 0]

@@ -102,6 +102,7 @@ def test_row_owned_combine_bit_exact(P, algo, m, l, n, bits, n_min, world, up):
         recv = torch.cat([sends[s].narrow(0, r * chunk, chunk) for s in range(world)])
         full = _rec_tensor(units * um * un * rw)
         shard.run_plan_torch(shard.a2a_unpack_plan(us, rows[r], rows[0].per, um, un, rw), full, recv)
+        torch.cuda.synchronize()  # torch's stream wrote `full`; the library runs on its own stream
         dc = P.DeviceMatrix(m, n, ctx)
         assert L.lib.mpgpu_fast_combine_rows(h, int(P.Algorithm[algo]), n_min, l, up, C.c_void_p(full.data_ptr()),
                                              rows[r].lo, rows[r].hi, C.byref(dc.m), None) == 0

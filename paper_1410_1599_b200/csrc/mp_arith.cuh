@@ -16,7 +16,12 @@
 // formats (L = 64 .. 288, up to 9216 bits) are compiled in separate translation units
 // (*_wide.cu, MPG_WIDE=1) where the same code runs as loops over local-memory arrays.
 #if MPG_WIDE
-#define MPG_UNROLL _Pragma("unroll 1")
+#ifndef MPG_WIDE_UNROLL
+#define MPG_WIDE_UNROLL 1
+#endif
+#define MPG_STR2_(x) #x
+#define MPG_STR_(x) MPG_STR2_(x)
+#define MPG_UNROLL _Pragma(MPG_STR_(unroll MPG_WIDE_UNROLL))
 #else
 #define MPG_UNROLL _Pragma("unroll")
 #endif

@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import subprocess
 import sys
 from pathlib import Path
@@ -19,7 +20,8 @@ LIB = PKG / "libmpgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu",
-           "gemm_wide.cu", "metrics_wide.cu", "elementwise_wide.cu", "lu_wide.cu"]
+           "gemm_wide.cu", "metrics_wide.cu"] + \
+    [f"{k}_wide{L}.cu" for k in ("elementwise", "lu") for L in (64, 128, 256, 288)]
 HEADERS = ["mp_arith.cuh", "kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -34,7 +36,7 @@ def _newest_dep() -> float:
 def _compile(src: str, force: bool) -> Path:
     obj = BUILD / (src + ".o")
     s = CSRC / src
-    srcs = [s] + ([CSRC / src.replace("_wide", "")] if "_wide" in src else [])  # *_wide.cu include *.cu
+    srcs = [s] + ([CSRC / re.sub(r"_wide\d*", "", src)] if "_wide" in src else [])  # *_wide*.cu include *.cu
     if (not force and obj.exists() and all(obj.stat().st_mtime >= x.stat().st_mtime for x in srcs)
             and obj.stat().st_mtime >= _newest_dep()):
         return obj

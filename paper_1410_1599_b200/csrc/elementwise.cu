@@ -437,10 +437,14 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);
 #if MPG_WIDE
+#ifdef MPG_WIDE_L  // one wide limb count per translation unit (compile time)
+MPG_INST(MPG_WIDE_L)
+#else
 MPG_INST(64)
 MPG_INST(128)
 MPG_INST(256)
 MPG_INST(288)
+#endif
 #else
 MPG_INST(1)
 MPG_INST(2)

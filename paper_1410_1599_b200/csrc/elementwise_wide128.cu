@@ -1,0 +1,5 @@
+// elementwise_wide128.cu -- the kernels of elementwise.cu for L = 128 limbs (wide format, limb loops
+// instead of full unrolling: mp_arith.cuh MPG_UNROLL); one limb count per translation unit.
+#define MPG_WIDE 1
+#define MPG_WIDE_L 128
+#include "elementwise.cu"

@@ -1,0 +1,5 @@
+// elementwise_wide288.cu -- the kernels of elementwise.cu for L = 288 limbs (wide format, limb loops
+// instead of full unrolling: mp_arith.cuh MPG_UNROLL); one limb count per translation unit.
+#define MPG_WIDE 1
+#define MPG_WIDE_L 288
+#include "elementwise.cu"

@@ -651,10 +651,14 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
   template void launch_lu_solve<L>(const uint32_t*, int64_t, const int64_t*, const uint32_t*, uint32_t*,        \
                                    uint32_t*, int, uint32_t*, int64_t*, int, int64_t, cudaStream_t);
 #if MPG_WIDE
+#ifdef MPG_WIDE_L  // one wide limb count per translation unit (compile time)
+MPG_LU_INST(MPG_WIDE_L)
+#else
 MPG_LU_INST(64)
 MPG_LU_INST(128)
 MPG_LU_INST(256)
 MPG_LU_INST(288)
+#endif
 #else
 MPG_LU_INST(1)
 MPG_LU_INST(2)

@@ -1,0 +1,5 @@
+// lu_wide288.cu -- the kernels of lu.cu for L = 288 limbs (wide format, limb loops
+// instead of full unrolling: mp_arith.cuh MPG_UNROLL); one limb count per translation unit.
+#define MPG_WIDE 1
+#define MPG_WIDE_L 288
+#include "lu.cu"

@@ -17,7 +17,7 @@
 // (*_wide.cu, MPG_WIDE=1) where the same code runs as loops over local-memory arrays.
 #if MPG_WIDE
 #ifndef MPG_WIDE_UNROLL
-#define MPG_WIDE_UNROLL 1
+#define MPG_WIDE_UNROLL 16  // measured: 2.5x faster than 1 on the 8192-bit Lotkin LU
 #endif
 #define MPG_STR2_(x) #x
 #define MPG_STR_(x) MPG_STR2_(x)

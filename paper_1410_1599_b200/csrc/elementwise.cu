@@ -14,6 +14,9 @@
 
 #include "kernels.h"
 #include "mp_arith.cuh"
+#if MPG_WIDE
+#include "wkern.cuh"
+#endif
 
 namespace mpg {
 
@@ -385,11 +388,19 @@ void launch_rec2soa(const uint32_t* rec, int64_t N, uint32_t* limbs, int32_t* ex
 template <int L>
 void launch_addsub(const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int is_sub, int sh,
                    uint32_t* err, cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_vec_op<L / 32>(is_sub ? 1 : 0, A, B, C, N, sh, err, st);
+#endif
   addsub_kernel<L><<<grid_for(N), NT, 0, st>>>(A, B, C, N, is_sub ? 1u : 0u, sh, err);
 }
 template <int L>
 void launch_vec_op(int op, const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int sh,
                    uint32_t* err, cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_vec_op<L / 32>(op, A, B, C, N, sh, err, st);
+#endif
   vec_op_kernel<L><<<grid_for(N), NT, 0, st>>>(op, A, B, C, N, sh, err);
 }
 template <int L>

@@ -20,6 +20,9 @@
 
 #include "kernels.h"
 #include "mp_arith.cuh"
+#if MPG_WIDE
+#include "wkern.cuh"
+#endif
 
 #ifndef MPG_MINB_8
 #define MPG_MINB_8 4
@@ -245,6 +248,10 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 
 template <int L>
 void launch_gemm(const GemmArgs& g, cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_gemm<L / 32>(g, st);
+#endif
   if constexpr (L == 8 || L == 16 || L == 32) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
     if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
   }

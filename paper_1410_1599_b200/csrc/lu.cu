@@ -18,6 +18,9 @@
 
 #include "kernels.h"
 #include "mp_arith.cuh"
+#if MPG_WIDE
+#include "wkern.cuh"
+#endif
 
 namespace mpg {
 
@@ -559,6 +562,11 @@ template <int L>
 int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting,
                          int64_t* piv, int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid,
                          cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled())
+      return wmp::launch_lu_panel<L / 32>(a, n, p, k, row_end, pivoting, piv, zp, sh, cand_key, cand_idx, max_grid, st);
+#endif
   constexpr int S = rec_stride(L);
   uint64_t* cand_cnt = reinterpret_cast<uint64_t*>(cand_idx + max_grid);
   static int max_blocks = 0;
@@ -627,6 +635,10 @@ template <int L>
 void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0, int64_t w, int sh,
                          cudaStream_t st) {
   if (w <= 0 || k <= 1) return;
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_trsm_panel<L / 32>(a, n, p, k, c0, w, sh, st);
+#endif
   trsm_l_panel_kernel<L><<<(int)((w + TRSM_TC - 1) / TRSM_TC), NT, 0, st>>>(a, n, p, k, c0, w, sh);
 }
 
@@ -634,6 +646,10 @@ template <int L>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const uint32_t* b, uint32_t* x,
                      uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, int exact, int64_t nrhs,
                      cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_lu_solve<L / 32>(f, n, piv_dev, b, x, scratch, sh, err, zp, exact, nrhs, st);
+#endif
   lu_solve_kernel<L><<<(unsigned)nrhs, NT, 0, st>>>(f, n, piv_dev, b, x, scratch, nullptr, sh, err, zp, exact);
 }
 

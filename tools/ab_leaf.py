@@ -1,0 +1,42 @@
+"""A/B timing of the leaf kernel: Winograd n=1024 (n_min 64) at several precisions,
+min over repetitions of the leaf and whole-step device times.  Select a library
+variant with MPGPU_LIB=paper_1410_1599_b200/_variants/<name>/libmpgpu.so.
+
+    python tools/ab_leaf.py [--bits 256 512 1024] [--reps 5] [--tag name]
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bits", type=int, nargs="+", default=[256, 512, 1024])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--n-min", type=int, default=64)
+    ap.add_argument("--algo", default="winograd")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--tag", default=os.environ.get("MPGPU_LIB", "default"))
+    a = ap.parse_args()
+    import paper_1410_1599_b200 as P
+    algo = P.Algorithm[a.algo]
+    for bits in a.bits:
+        ctx = P.PrecisionContext(bits)
+        A = P.gen_uniform_full(a.n, a.n, 1, ctx).to_device()
+        B = P.gen_uniform_full(a.n, a.n, 2, ctx).to_device()
+        C = P.DeviceMatrix(a.n, a.n, ctx)
+        leaf, dev = [], []
+        for _ in range(a.reps + 1):
+            st = P.gemm_into(algo, a.n_min if algo != P.Algorithm.simple else 0, A, B, C)
+            leaf.append(st.leaf_ms)
+            dev.append(st.device_ms)
+        print(json.dumps({"tag": a.tag, "algo": a.algo, "n": a.n, "bits": bits,
+                          "leaf_ms": min(leaf[1:]), "device_ms": min(dev[1:])}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

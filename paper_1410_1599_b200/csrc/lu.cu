@@ -565,7 +565,7 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
 #if MPG_WIDE
   if constexpr (L > 32)
     if (wmp::enabled())
-      return wmp::launch_lu_panel<L / 32>(a, n, p, k, row_end, pivoting, piv, zp, sh, cand_key, cand_idx, max_grid, st);
+      return wmp::launch_lu_panel<L / 32>(a, n, p, k, row_end, pivoting, piv, zp, sh, st);
 #endif
   constexpr int S = rec_stride(L);
   uint64_t* cand_cnt = reinterpret_cast<uint64_t*>(cand_idx + max_grid);

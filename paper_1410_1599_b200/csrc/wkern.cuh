@@ -143,6 +143,10 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
 }
 
 // ---- LU (lu.cu contracts) ------------------------------------------------------
+// The LU kernels are cooperative: every parallel phase (divisions, rank-1 updates,
+// triangular-solve steps) is spread over all warps of a grid that fills the GPU, with a
+// grid barrier between dependent phases -- an 8192-bit multiply-add takes tens of
+// microseconds in one warp, so the per-column work must not be confined to a few CTAs.
 __device__ __forceinline__ uint64_t wmag_key(uint32_t e, uint32_t top) {
   return e == (uint32_t)EXP_ZERO ? 0ull : (((uint64_t)(e ^ 0x80000000u)) << 32) | top;
 }
@@ -158,15 +162,43 @@ __device__ __forceinline__ void wpiv_combine(uint64_t& k, int64_t& i, int& c, ui
   }
 }
 
-// whole-panel factorisation in one cooperative launch (lu.cu lu_panel_coop_kernel):
-// per pivot column d -- (pivoting) candidate reduction, swap, grid.sync; one warp per
-// row divides (multiplier), then one warp per (row, column) applies the rank-1
-// update of the CTA's rows; next column's candidates; grid.sync.
+// a_ij = RN(a_ij - RN(l * u)) for the record at xr (blocklu.hpp:51-52, 66-67)
+template <int V>
+__device__ __forceinline__ void sub_prod(uint32_t* xr, const uint32_t* lr, const uint32_t* ur, int sh,
+                                         const Scratch<V>& sc) {
+  W<V> l, u, pr, x;
+  load_w<V>(lr, l);
+  load_w<V>(ur, u);
+  mul_w<V>(l, u, sh, sc, pr);
+  load_w<V>(xr, x);
+  add_w<V>(x, pr, 1u, sh, x);
+  store_w<V>(xr, x);
+}
+
+// co-resident grid size for a cooperative kernel, capped by the useful warps
+template <class K>
+inline int coop_grid(K kern, size_t smem, int64_t want_warps) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  set_smem(kern, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WNT, smem);
+  int64_t g = (want_warps + WWARPS - 1) / WWARPS;
+  const int64_t cap = (int64_t)per_sm * sms;
+  if (const char* e = std::getenv("MPGPU_LU_COOP_GRID")) g = std::min<int64_t>(g, std::atoll(e));
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// whole-panel factorisation [p, p+k) x rows [p, row_end) in one cooperative launch
+// (lu.cu lu_panel_coop_kernel).  Per pivot column d: (pivoting) every CTA reduces the
+// column's magnitude keys itself -- identical pivot everywhere -- CTA 0 swaps the
+// panel rows, barrier; multipliers (one warp per row, all warps of the grid), barrier;
+// rank-1 update (one warp per element, all warps), barrier.
 template <int V>
 __global__ void __launch_bounds__(WNT) lu_panel_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k,
                                                        int64_t row_end, int pivoting, int64_t* piv, int64_t* zp,
-                                                       int sh, uint64_t* cand_key, int64_t* cand_idx,
-                                                       uint64_t* cand_cnt) {
+                                                       int sh) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   constexpr int L = 32 * V, S = rec_stride(L);
@@ -176,82 +208,46 @@ __global__ void __launch_bounds__(WNT) lu_panel_kernel(uint32_t* a, int64_t n, i
   __shared__ int s_wc[WWARPS];
   __shared__ int64_t s_piv;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t rows_all = row_end - p;
-  const int64_t chunk = (rows_all + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = p + (int64_t)blockIdx.x * chunk;
-  const int64_t hi = min(row_end, lo + chunk);
-  auto block_reduce_store = [&](uint64_t bk, int64_t bi, int bc) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_xor_sync(FULL, bk, o);
-      const int64_t i2 = __shfl_xor_sync(FULL, bi, o);
-      const int c2 = __shfl_xor_sync(FULL, bc, o);
-      wpiv_combine(bk, bi, bc, k2, i2, c2);
-    }
-    if (lane == 0) {
-      s_wk[wid] = bk;
-      s_wi[wid] = bi;
-      s_wc[wid] = bc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < WWARPS; ++w) wpiv_combine(bk, bi, bc, s_wk[w], s_wi[w], s_wc[w]);
-      cand_key[blockIdx.x] = bk;
-      cand_idx[blockIdx.x] = bi;
-      cand_cnt[blockIdx.x] = (uint64_t)bc;
-    }
-    __syncthreads();
-  };
-  auto candidates = [&](int64_t col, int64_t from) {
-    uint64_t bk = 0;
-    int64_t bi = INT64_MAX;
-    int bc = 0;
-    for (int64_t i = max(from, lo) + tid; i < hi; i += WNT) {
-      const uint32_t* r = a + (i * n + col) * S;
-      wpiv_combine(bk, bi, bc, wmag_key(r[L], r[L - 1]), i, 1);
-    }
-    block_reduce_store(bk, bi, bc);
-  };
-  if (pivoting) {
-    candidates(p, p);
-    grid.sync();
-  }
+  const int64_t gw = gwarp(), NW = nwarps();
   for (int64_t d = p; d < p + k; ++d) {
     if (pivoting) {
-      uint64_t gk = 0;
-      int64_t gi = INT64_MAX;
-      int gc = 0;
-      for (unsigned b = tid; b < gridDim.x; b += WNT) wpiv_combine(gk, gi, gc, cand_key[b], cand_idx[b], (int)cand_cnt[b]);
+      uint64_t bk = 0;
+      int64_t bi = INT64_MAX;
+      int bc = 0;
+      for (int64_t i = d + tid; i < row_end; i += WNT) {
+        const uint32_t* r = a + (i * n + d) * S;
+        wpiv_combine(bk, bi, bc, wmag_key(r[L], r[L - 1]), i, 1);
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(FULL, gk, o);
-        const int64_t i2 = __shfl_xor_sync(FULL, gi, o);
-        const int c2 = __shfl_xor_sync(FULL, gc, o);
-        wpiv_combine(gk, gi, gc, k2, i2, c2);
+        const uint64_t k2 = __shfl_xor_sync(FULL, bk, o);
+        const int64_t i2 = __shfl_xor_sync(FULL, bi, o);
+        const int c2 = __shfl_xor_sync(FULL, bc, o);
+        wpiv_combine(bk, bi, bc, k2, i2, c2);
       }
       if (lane == 0) {
-        s_wk[wid] = gk;
-        s_wi[wid] = gi;
-        s_wc[wid] = gc;
+        s_wk[wid] = bk;
+        s_wi[wid] = bi;
+        s_wc[wid] = bc;
       }
       __syncthreads();
       if (wid == 0) {
-        for (int w = 1; w < WWARPS; ++w) wpiv_combine(gk, gi, gc, s_wk[w], s_wi[w], s_wc[w]);
-        if (gc > 1) {  // rows sharing the winning compact key: full comparison (first max wins)
+        for (int w = 1; w < WWARPS; ++w) wpiv_combine(bk, bi, bc, s_wk[w], s_wi[w], s_wc[w]);
+        if (bc > 1) {  // rows sharing the winning compact key: full comparison (first max wins)
           W<V> rv, x;
           int64_t r = -1;
           for (int64_t i = d; i < row_end; ++i) {
             const uint32_t* q = a + (i * n + d) * S;
-            if (wmag_key(q[L], q[L - 1]) != gk) continue;
+            if (wmag_key(q[L], q[L - 1]) != bk) continue;
             load_w<V>(q, x);
             if (r < 0 || cmpabs_w<V>(x, rv) > 0) {
               rv = x;
               r = i;
             }
           }
-          gi = r;
+          bi = r;
         }
-        if (lane == 0) s_piv = gi;
+        if (lane == 0) s_piv = bi;
       }
       __syncthreads();
       const int64_t r = s_piv;
@@ -275,35 +271,25 @@ __global__ void __launch_bounds__(WNT) lu_panel_kernel(uint32_t* a, int64_t n, i
       if (blockIdx.x == 0 && tid == 0) *zp = d + 1;
       return;
     }
-    const int64_t r0 = max(d + 1, lo);
-    const int64_t nr = hi - r0;
-    if (nr > 0) {
+    const int64_t rows = row_end - d - 1;
+    if (rows <= 0) break;
+    {
       W<V> pv;
       load_w<V>(a + (d * n + d) * S, pv);
-      for (int64_t t = wid; t < nr; t += WWARPS) {
+      for (int64_t t = gw; t < rows; t += NW) {
         W<V> x, q;
-        uint32_t* xr = a + ((r0 + t) * n + d) * S;
+        uint32_t* xr = a + ((d + 1 + t) * n + d) * S;
         load_w<V>(xr, x);
         div_w<V>(x, pv, sh, sc, q);
         store_w<V>(xr, q);
       }
-      __syncthreads();
-      const int64_t w = p + k - d - 1;
-      for (int64_t t = wid; t < nr * w; t += WWARPS) {
-        const int64_t rr = t / w, j = d + 1 + t % w;
-        W<V> l, u, pr, x;
-        load_w<V>(a + ((r0 + rr) * n + d) * S, l);
-        load_w<V>(a + (d * n + j) * S, u);
-        mul_w<V>(l, u, sh, sc, pr);
-        uint32_t* xr = a + ((r0 + rr) * n + j) * S;
-        load_w<V>(xr, x);
-        add_w<V>(x, pr, 1u, sh, x);
-        store_w<V>(xr, x);
-      }
     }
-    if (pivoting && d + 1 < p + k) {
-      __syncthreads();
-      candidates(d + 1, d + 1);
+    const int64_t w = p + k - d - 1;
+    if (w <= 0) break;
+    grid.sync();
+    for (int64_t t = gw; t < rows * w; t += NW) {
+      const int64_t i = d + 1 + t / w, j = d + 1 + t % w;
+      sub_prod<V>(a + (i * n + j) * S, a + (i * n + d) * S, a + (d * n + j) * S, sh, sc);
     }
     grid.sync();
   }
@@ -311,55 +297,34 @@ __global__ void __launch_bounds__(WNT) lu_panel_kernel(uint32_t* a, int64_t n, i
 
 template <int V>
 int launch_lu_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting, int64_t* piv,
-                    int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid, cudaStream_t st) {
-  uint64_t* cand_cnt = reinterpret_cast<uint64_t*>(cand_idx + max_grid);
-  static int max_blocks = 0;
+                    int64_t* zp, int sh, cudaStream_t st) {
   const size_t smem = smem_bytes<V>();
-  if (!max_blocks) {
-    set_smem(lu_panel_kernel<V>, smem);
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel<V>, WNT, smem);
-    max_blocks = per_sm * sms;
-  }
   const int64_t rows = row_end - p;
-  // a few rows per CTA: every warp divides at most one row per column
-  int64_t grid = (rows + WWARPS - 1) / WWARPS;
-  if (grid > max_blocks) grid = max_blocks;
-  if (const char* g = std::getenv("MPGPU_LU_COOP_GRID")) grid = std::min<int64_t>(grid, std::atoll(g));
-  if (grid > max_grid) grid = max_grid;
-  if (grid < 1) grid = 1;
-  void* args[] = {&a, &n, &p, &k, &row_end, &pivoting, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt};
+  int grid = coop_grid(lu_panel_kernel<V>, smem, rows * std::min<int64_t>(k, rows));
+  void* args[] = {&a, &n, &p, &k, &row_end, &pivoting, &piv, &zp, (void*)&sh};
   const cudaError_t e =
       cudaLaunchCooperativeKernel((void*)lu_panel_kernel<V>, dim3((unsigned)grid), dim3(WNT), args, smem, st);
   return e == cudaSuccess ? 0 : -1;
 }
 
-// trsm_unit_lower over a panel (lu.cu trsm_l_panel_kernel): each CTA owns TC columns
-// of U12 and sweeps s = p .. p+k-2, one warp per (row, column) element per step
+// trsm_unit_lower over a panel (lu.cu trsm_l_panel_kernel): step s = p .. p+k-2 updates
+// rows (s, p+k) x cols [c0, c0+w) -- one warp per element over the whole grid -- then a
+// grid barrier; per element the updates arrive in s-ascending order (blocklu.hpp:60-69).
 template <int V>
 __global__ void __launch_bounds__(WNT) trsm_panel_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0,
-                                                         int64_t w, int sh, int TC) {
+                                                         int64_t w, int sh) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   constexpr int S = rec_stride(32 * V);
   const Scratch<V> sc = my_scratch<V>();
-  const int wid = threadIdx.x >> 5;
-  const int64_t j0 = c0 + (int64_t)blockIdx.x * TC;
-  const int tc = (int)(c0 + w - j0 < TC ? c0 + w - j0 : TC);
+  const int64_t gw = gwarp(), NW = nwarps();
   for (int64_t s = p; s + 1 < p + k; ++s) {
     const int64_t rows = p + k - s - 1;
-    for (int64_t t = wid; t < rows * tc; t += WWARPS) {
-      const int64_t i = s + 1 + t / tc, j = j0 + t % tc;
-      W<V> l, u, pr, x;
-      load_w<V>(a + (i * n + s) * S, l);
-      load_w<V>(a + (s * n + j) * S, u);
-      mul_w<V>(l, u, sh, sc, pr);
-      uint32_t* xr = a + (i * n + j) * S;
-      load_w<V>(xr, x);
-      add_w<V>(x, pr, 1u, sh, x);
-      store_w<V>(xr, x);
+    for (int64_t t = gw; t < rows * w; t += NW) {
+      const int64_t i = s + 1 + t / w, j = c0 + t % w;
+      sub_prod<V>(a + (i * n + j) * S, a + (i * n + s) * S, a + (s * n + j) * S, sh, sc);
     }
-    __syncthreads();
+    grid.sync();
   }
 }
 
@@ -367,105 +332,81 @@ template <int V>
 void launch_trsm_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0, int64_t w, int sh,
                        cudaStream_t st) {
   if (w <= 0 || k <= 1) return;
-  constexpr int TC = 2;
-  set_smem(trsm_panel_kernel<V>, smem_bytes<V>());
-  trsm_panel_kernel<V><<<(unsigned)((w + TC - 1) / TC), WNT, smem_bytes<V>(), st>>>(a, n, p, k, c0, w, sh, TC);
+  const size_t smem = smem_bytes<V>();
+  int grid = coop_grid(trsm_panel_kernel<V>, smem, (k - 1) * w);
+  void* args[] = {&a, &n, &p, &k, &c0, &w, (void*)&sh};
+  cudaLaunchCooperativeKernel((void*)trsm_panel_kernel<V>, dim3((unsigned)grid), dim3(WNT), args, smem, st);
 }
 
-// Ly = Pb, Ux = y (lu.cu lu_solve_kernel): one CTA per right-hand side, warps over rows;
-// the exact back substitution accumulates each row's products in s-ascending order
-// (blocklu.hpp:235-238) in warp 0.
+// Ly = Pb, Ux = y for nrhs right-hand sides (lu.cu lu_solve_kernel), cooperative: the
+// parallel steps -- forward updates, back-substitution products / updates -- run over
+// (right-hand side, row) pairs on all warps of the grid; the exact back substitution's
+// s-ascending accumulation of each row (blocklu.hpp:235-238) runs in one warp per
+// right-hand side.  Scratch: 2n records per right-hand side (y, products).
 template <int V>
 __global__ void __launch_bounds__(WNT) lu_solve_kernel(const uint32_t* f, int64_t n, const int64_t* piv,
                                                        const uint32_t* b, uint32_t* x, uint32_t* y, int sh,
-                                                       uint32_t* err, int64_t* zp, int exact) {
+                                                       uint32_t* err, int64_t* zp, int exact, int64_t nrhs) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   constexpr int S = rec_stride(32 * V), CH = S / 4;
   const Scratch<V> sc = my_scratch<V>();
-  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  b += (int64_t)blockIdx.x * n * S;
-  x += (int64_t)blockIdx.x * n * S;
-  y += (int64_t)blockIdx.x * 2 * n * S;
-  uint32_t* tmp = y + n * S;
-  for (int64_t t = tid; t < n * CH; t += WNT) reinterpret_cast<uint4*>(y)[t] = reinterpret_cast<const uint4*>(b)[t];
-  __syncthreads();
-  if (piv && tid == 0) {
-    for (int64_t d = 0; d < n; ++d) {
-      const int64_t r = piv[d];
-      if (r != d)
-        for (int w = 0; w < CH; ++w) {
-          uint4* pp = reinterpret_cast<uint4*>(y + d * S) + w;
-          uint4* qq = reinterpret_cast<uint4*>(y + r * S) + w;
-          const uint4 t = *pp;
-          *pp = *qq;
-          *qq = t;
-        }
-    }
+  const int lane = lane_id();
+  const int64_t gw = gwarp(), NW = nwarps();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, NT = (int64_t)gridDim.x * blockDim.x;
+  auto Y = [&](int64_t r) { return y + r * 2 * n * S; };
+  auto T = [&](int64_t r) { return y + r * 2 * n * S + n * S; };
+  for (int64_t t = gt; t < nrhs * n * CH; t += NT) {
+    const int64_t r = t / (n * CH), q = t - r * n * CH;
+    reinterpret_cast<uint4*>(Y(r))[q] = reinterpret_cast<const uint4*>(b + r * n * S)[q];
   }
-  __syncthreads();
-  for (int64_t s = 0; s < n; ++s) {
-    W<V> ys;
-    load_w<V>(y + s * S, ys);
-    for (int64_t i = s + 1 + wid; i < n; i += WWARPS) {
-      W<V> l, pr, acc;
-      load_w<V>(f + (i * n + s) * S, l);
-      mul_w<V>(l, ys, sh, sc, pr);
-      load_w<V>(y + i * S, acc);
-      add_w<V>(acc, pr, 1u, sh, acc);
-      store_w<V>(y + i * S, acc);
-    }
-    __syncthreads();
+  grid.sync();
+  if (piv) {
+    for (int64_t r = gt; r < nrhs; r += NT)
+      for (int64_t d = 0; d < n; ++d) {
+        const int64_t pr = piv[d];
+        if (pr != d)
+          for (int w = 0; w < CH; ++w) {
+            uint4* pp = reinterpret_cast<uint4*>(Y(r) + d * S) + w;
+            uint4* qq = reinterpret_cast<uint4*>(Y(r) + pr * S) + w;
+            const uint4 tv = *pp;
+            *pp = *qq;
+            *qq = tv;
+          }
+      }
+    grid.sync();
   }
-  __shared__ int s_stop;
-  if (!exact) {
-    for (int64_t ii = n - 1; ii >= 0; --ii) {
-      if (wid == 0) {
-        W<V> acc, dd, q;
-        load_w<V>(y + ii * S, acc);
-        load_w<V>(f + (ii * n + ii) * S, dd);
-        if (dd.e == EXP_ZERO) {
-          if (lane == 0 && *zp == 0) *zp = ii + 1;
-          zero_w<V>(q);
-        } else {
-          div_w<V>(acc, dd, sh, sc, q);
-        }
-        if (lane == 0 && exp_out_of_range(q.e)) atomicOr(err, ERR_EXP_RANGE);
-        store_w<V>(x + ii * S, q);
-        if (lane == 0) s_stop = dd.e == EXP_ZERO;
-      }
-      __syncthreads();
-      if (s_stop) return;
-      W<V> xs;
-      load_w<V>(x + ii * S, xs);
-      for (int64_t i = wid; i < ii; i += WWARPS) {
-        W<V> u, pr, acc;
-        load_w<V>(f + (i * n + ii) * S, u);
-        mul_w<V>(u, xs, sh, sc, pr);
-        load_w<V>(y + i * S, acc);
-        add_w<V>(acc, pr, 1u, sh, acc);
-        store_w<V>(y + i * S, acc);
-      }
-      __syncthreads();
+  // forward substitution, column sweep (per element s ascending)
+  for (int64_t s = 0; s + 1 < n; ++s) {
+    const int64_t rows = n - s - 1;
+    for (int64_t t = gw; t < nrhs * rows; t += NW) {
+      const int64_t r = t / rows, i = s + 1 + (t - r * rows);
+      sub_prod<V>(Y(r) + i * S, f + (i * n + s) * S, Y(r) + s * S, sh, sc);
     }
-    return;
+    grid.sync();
   }
   for (int64_t ii = n - 1; ii >= 0; --ii) {
-    for (int64_t s = ii + 1 + wid; s < n; s += WWARPS) {
-      W<V> u, xs, pr;
-      load_w<V>(f + (ii * n + s) * S, u);
-      load_w<V>(x + s * S, xs);
-      mul_w<V>(u, xs, sh, sc, pr);
-      store_w<V>(tmp + s * S, pr);
-    }
-    __syncthreads();
-    if (wid == 0) {
-      W<V> acc;
-      load_w<V>(y + ii * S, acc);
-      for (int64_t s = ii + 1; s < n; ++s) {
-        W<V> pr;
-        load_w<V>(tmp + s * S, pr);
-        add_w<V>(acc, pr, 1u, sh, acc);
+    if (exact) {  // products of row ii, then the s-ascending chain
+      const int64_t cnt = n - ii - 1;
+      for (int64_t t = gw; t < nrhs * cnt; t += NW) {
+        const int64_t r = t / cnt, s = ii + 1 + (t - r * cnt);
+        W<V> u, xs, pr;
+        load_w<V>(f + (ii * n + s) * S, u);
+        load_w<V>(x + (r * n + s) * S, xs);
+        mul_w<V>(u, xs, sh, sc, pr);
+        store_w<V>(T(r) + s * S, pr);
       }
-      W<V> dd, q;
+      if (cnt > 0) grid.sync();
+    }
+    for (int64_t r = gw; r < nrhs; r += NW) {
+      W<V> acc, dd, q;
+      load_w<V>(Y(r) + ii * S, acc);
+      if (exact)
+        for (int64_t s = ii + 1; s < n; ++s) {
+          W<V> pr;
+          load_w<V>(T(r) + s * S, pr);
+          add_w<V>(acc, pr, 1u, sh, acc);
+        }
       load_w<V>(f + (ii * n + ii) * S, dd);
       if (dd.e == EXP_ZERO) {
         if (lane == 0 && *zp == 0) *zp = ii + 1;
@@ -474,11 +415,17 @@ __global__ void __launch_bounds__(WNT) lu_solve_kernel(const uint32_t* f, int64_
         div_w<V>(acc, dd, sh, sc, q);
       }
       if (lane == 0 && exp_out_of_range(q.e)) atomicOr(err, ERR_EXP_RANGE);
-      store_w<V>(x + ii * S, q);
-      if (lane == 0) s_stop = dd.e == EXP_ZERO;
+      store_w<V>(x + (r * n + ii) * S, q);
     }
-    __syncthreads();
-    if (s_stop) return;
+    grid.sync();
+    if (*(volatile int64_t*)zp) return;
+    if (!exact && ii > 0) {  // column-oriented: y_i -= RN(u_i,ii * x_ii), i < ii
+      for (int64_t t = gw; t < nrhs * ii; t += NW) {
+        const int64_t r = t / ii, i = t - r * ii;
+        sub_prod<V>(Y(r) + i * S, f + (i * n + ii) * S, x + (r * n + ii) * S, sh, sc);
+      }
+      grid.sync();
+    }
   }
 }
 
@@ -486,8 +433,10 @@ template <int V>
 void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv, const uint32_t* b, uint32_t* x,
                      uint32_t* scratch, int sh, uint32_t* err, int64_t* zp, int exact, int64_t nrhs,
                      cudaStream_t st) {
-  set_smem(lu_solve_kernel<V>, smem_bytes<V>());
-  lu_solve_kernel<V><<<(unsigned)nrhs, WNT, smem_bytes<V>(), st>>>(f, n, piv, b, x, scratch, sh, err, zp, exact);
+  const size_t smem = smem_bytes<V>();
+  int grid = coop_grid(lu_solve_kernel<V>, smem, nrhs * n);
+  void* args[] = {&f, &n, &piv, &b, &x, &scratch, (void*)&sh, &err, &zp, (void*)&exact, &nrhs};
+  cudaLaunchCooperativeKernel((void*)lu_solve_kernel<V>, dim3((unsigned)grid), dim3(WNT), args, smem, st);
 }
 
 }  // namespace wmp

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu",
            "gemm_wide.cu", "metrics_wide.cu"] + \
     [f"{k}_wide{L}.cu" for k in ("elementwise", "lu") for L in (64, 128, 256, 288)]
-HEADERS = ["mp_arith.cuh", "kernels.h"]
+HEADERS = ["mp_arith.cuh", "kernels.h", "wmp.cuh", "wkern.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-I" + str(ROOT / "include")]

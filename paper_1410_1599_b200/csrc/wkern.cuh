@@ -101,15 +101,20 @@ __global__ void __launch_bounds__(WNT) gemm_kernel(const GemmArgs g) {
     zero_w<V>(acc, 1u);  // -0: RN(-0 + x) == x (gemm.cu)
     zero_w<V>(pacc, 1u);
     int next_b = g.kb;
+    W<V> na, nb;  // operands of the next k, loaded one step ahead (latency-bound loop)
+    load_w<V>(A, na);
+    load_w<V>(B, nb);
     for (int k = 0; k < g.l; ++k) {
       if (FOLD && k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
         add_w<V>(acc, pacc, 0u, g.sh, acc);
         zero_w<V>(pacc, 1u);
         next_b += g.kb;
       }
-      W<V> a, b, t;
-      load_w<V>(A + (int64_t)k * S, a);
-      load_w<V>(B + (int64_t)k * g.ldb * S, b);
+      W<V> a = na, b = nb, t;
+      if (k + 1 < g.l) {
+        load_w<V>(A + (int64_t)(k + 1) * S, na);
+        load_w<V>(B + (int64_t)(k + 1) * g.ldb * S, nb);
+      }
       mul_w<V>(a, b, g.sh, sc, t);
       add_w<V>(pacc, t, 0u, g.sh, pacc);
     }
@@ -401,12 +406,15 @@ __global__ void __launch_bounds__(WNT) lu_solve_kernel(const uint32_t* f, int64_
     for (int64_t r = gw; r < nrhs; r += NW) {
       W<V> acc, dd, q;
       load_w<V>(Y(r) + ii * S, acc);
-      if (exact)
+      if (exact && ii + 1 < n) {  // the chain, with the next product loaded one step ahead
+        W<V> nx;
+        load_w<V>(T(r) + (ii + 1) * S, nx);
         for (int64_t s = ii + 1; s < n; ++s) {
-          W<V> pr;
-          load_w<V>(T(r) + s * S, pr);
+          const W<V> pr = nx;
+          if (s + 1 < n) load_w<V>(T(r) + (s + 1) * S, nx);
           add_w<V>(acc, pr, 1u, sh, acc);
         }
+      }
       load_w<V>(f + (ii * n + ii) * S, dd);
       if (dd.e == EXP_ZERO) {
         if (lane == 0 && *zp == 0) *zp = ii + 1;

@@ -399,15 +399,22 @@ __device__ __forceinline__ void add_w(const W<V>& x, const W<V>& y, uint32_t neg
 }
 
 // ---------------------------------------------------------------------------
-// full L x L -> 2L limb product of the staged operands, exact.  Lane l accumulates
-// the columns t = l + 32 j (j < 2V) in three words each (strided: every lane gets a
-// balanced share of the triangular column lengths), the column sums go through shared
-// memory to a blocked layout (lane l: limbs [2 V l, 2 V l + 2V)) where carries are
-// resolved inside the lane and across lanes (shuffle + lookahead).
+// Limb product of x and y, column-wise over the warp.  FULL: all 2L columns, exact.
+// SHORT: only the columns t >= L-2 (i + j >= L-2 -- the truncated product of
+// mp_arith.cuh mul_high_g, (L^2 + 3L - 2)/2 limb products); the omitted part is below
+// L-1 units of limb L-1.  Lane l accumulates the columns t = c0 + l + 32 j in three
+// words each (strided: every lane gets a balanced share of the triangular column
+// lengths), the column sums go through shared memory to a blocked layout where carries
+// are resolved inside the lane and across lanes (shuffle + lookahead).
+// FULL:  P[q] = product limb 2 V l + q (q < 2V).
+// SHORT: P[q] = product limb L + V l + q (q < V); g1 / g0 = limbs L-1 / L-2 (uniform).
 // ---------------------------------------------------------------------------
-template <int V>
-__device__ __forceinline__ void product_w(const W<V>& x, const W<V>& y, const Scratch<V>& sc, uint32_t (&P)[2 * V]) {
+template <int V, bool SHORT>
+__device__ __forceinline__ void product_w(const W<V>& x, const W<V>& y, const Scratch<V>& sc,
+                                          uint32_t (&P)[2 * V], uint32_t& g1, uint32_t& g0) {
   constexpr int L = 32 * V;
+  constexpr int C0 = SHORT ? L - 2 : 0;      // first column computed
+  constexpr int NB = SHORT ? V + 1 : 2 * V;  // blocks of 32 columns
   const int lane = lane_id();
   __syncwarp();
 #pragma unroll
@@ -424,15 +431,18 @@ __device__ __forceinline__ void product_w(const W<V>& x, const W<V>& y, const Sc
     sc.b[40 + L + t] = 0;
   }
   __syncwarp();
-  uint32_t acc[2 * V][3];
+  constexpr int NC = 32 * NB;  // columns stored (relative to C0)
 #pragma unroll
-  for (int j = 0; j < 2 * V; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0;
-#pragma unroll
-  for (int j = 0; j < 2 * V; ++j) {
-    const int c = 32 * j;                        // this block's first column
+  for (int j = 0; j < NB; ++j) {
+    const int c = C0 + 32 * j;  // this block's first column
     const int ilo = c - (L - 1) > 0 ? c - (L - 1) : 0;
     const int ihi = c + 31 < L - 1 ? c + 31 : L - 1;
     const int t = c + lane;
+    // four independent three-word accumulators (one per term of a group of four):
+    // the carry chains of consecutive terms do not serialise
+    uint32_t acc[4][3];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = acc[u][2] = 0;
 #pragma unroll 2
     for (int i = ilo & ~3; i <= ihi; i += 4) {
       const uint4 a4 = *reinterpret_cast<const uint4*>(sc.a + 4 + i);
@@ -441,62 +451,104 @@ __device__ __forceinline__ void product_w(const W<V>& x, const W<V>& y, const Sc
       for (int u = 0; u < 4; ++u) {
         const uint32_t bv = sc.b[40 + t - i - u];
         const uint64_t pr = (uint64_t)av[u] * bv;
-        asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[j][0]) : "r"((uint32_t)pr));
-        asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[j][1]) : "r"((uint32_t)(pr >> 32)));
-        asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[j][2]));
+        asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[u][0]) : "r"((uint32_t)pr));
+        asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[u][1]) : "r"((uint32_t)(pr >> 32)));
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[u][2]));
       }
     }
-  }
-  __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 2 * V; ++j) {
-    const int t = lane + 32 * j;
-    sc.col[t] = acc[j][0];
-    sc.col[2 * L + t] = acc[j][1];
-    sc.col[4 * L + t] = acc[j][2];
+    for (int u = 1; u < 4; ++u) {
+      asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[0][0]) : "r"(acc[u][0]));
+      asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[0][1]) : "r"(acc[u][1]));
+      asm volatile("addc.u32 %0, %0, %1;" : "+r"(acc[0][2]) : "r"(acc[u][2]));
+    }
+    sc.col[lane + 32 * j] = acc[0][0];
+    sc.col[NC + lane + 32 * j] = acc[0][1];
+    sc.col[2 * NC + lane + 32 * j] = acc[0][2];
   }
   __syncwarp();
+  constexpr int NQ = SHORT ? V : 2 * V;  // limbs resolved per lane
+  const int base = SHORT ? 2 + V * lane : 2 * V * lane;
   uint32_t k0 = 0, k1 = 0;
-#pragma unroll
-  for (int q = 0; q < 2 * V; ++q) {
-    const int t = 2 * V * lane + q;
-    const uint32_t c0 = sc.col[t], c1 = sc.col[2 * L + t], c2 = sc.col[4 * L + t];
+  auto step = [&](int t) -> uint32_t {
+    const uint32_t c0 = sc.col[t], c1 = sc.col[NC + t], c2 = sc.col[2 * NC + t];
     uint32_t s0, s1, s2;
     asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(s0) : "r"(c0), "r"(k0));
     asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(s1) : "r"(c1), "r"(k1));
     asm volatile("addc.u32 %0, %1, 0;" : "=r"(s2) : "r"(c2));
-    P[q] = s0;
     k0 = s1;
     k1 = s2;
+    return s0;
+  };
+  uint32_t lg0 = 0, lg1 = 0;
+  if (SHORT && lane == 0) {  // the two guard columns L-2, L-1 first
+    lg0 = step(0);
+    lg1 = step(1);
   }
-  // add the previous lane's carry (two words) at this lane's limb 0, then 1-bit carries
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) P[q] = step(base + q);
+  // add the previous lane's carry (two words) at this lane's first limb, then 1-bit carries
   uint32_t p0 = __shfl_up_sync(FULL, k0, 1), p1 = __shfl_up_sync(FULL, k1, 1);
   if (lane == 0) p0 = p1 = 0;
   uint32_t g;
   asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(P[0]) : "r"(p0));
   asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(P[1]) : "r"(p1));
 #pragma unroll
-  for (int q = 2; q < 2 * V; ++q) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(P[q]));
+  for (int q = 2; q < NQ; ++q) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(P[q]));
   asm volatile("addc.u32 %0, 0, 0;" : "=r"(g));
+  uint32_t pr = 1u;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) pr &= (P[q] == 0xFFFFFFFFu) ? 1u : 0u;
   uint32_t cout;
-  const uint32_t ci = lookahead(g, lane > 0 ? all_ones<2 * V>(P) : 0u, 0u, cout);
-  add_bit<2 * V>(P, ci);
+  const uint32_t ci = lookahead(g, lane > 0 ? pr : 0u, 0u, cout);
+  asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(P[0]) : "r"(ci));
+#pragma unroll
+  for (int q = 1; q < NQ; ++q) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(P[q]));
+  g1 = __shfl_sync(FULL, lg1, 0);
+  g0 = __shfl_sync(FULL, lg0, 0);
   __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
-// z = RN_p(x * y)  (mpfr_mul; mp_arith.cuh mp_mul) from the exact full product
+// z = RN_p(x * y)  (mpfr_mul; mp_arith.cuh mp_mul).  The short product decides the
+// rounding unless the true guard limb may lie near a rounding boundary (mpfr_mul's
+// mulhigh strategy, as mp_mul_g); otherwise the exact full product is formed.
 // ---------------------------------------------------------------------------
 template <int V>
 __device__ __forceinline__ void mul_w(const W<V>& x, const W<V>& y, int sh, const Scratch<V>& sc, W<V>& z) {
+  constexpr int L = 32 * V;
   const int lane = lane_id();
   const uint32_t zs = x.s ^ y.s;
+  z.s = zs;
   if (x.e == EXP_ZERO || y.e == EXP_ZERO) {
     zero_w<V>(z, zs);
     return;
   }
-  uint32_t P[2 * V];
-  product_w<V>(x, y, sc, P);
+  uint32_t P[2 * V], g1, g0;
+  {
+    product_w<V, true>(x, y, sc, P, g1, g0);
+    const uint32_t top = __shfl_sync(FULL, P[V - 1], 31);
+    const uint32_t t1 = (top >> 31) ^ 1u;
+    const uint32_t gt = __funnelshift_l(g0, g1, t1);
+    // the true guard limb lies in [gt, gt + 2L)
+    const bool down = gt < 0x80000000u - 2u * L;
+    const bool up = gt > 0x80000000u && gt < 0xFFFFFFFFu - 2u * L;
+    const bool ok = sh == 0 ? (down | up) : (gt != 0 && gt < 0xFFFFFFFFu - 2u * L);
+    if (ok) {
+      uint32_t prv = __shfl_up_sync(FULL, P[V - 1], 1);
+      if (lane == 0) prv = g1;
+#pragma unroll
+      for (int j = V - 1; j > 0; --j) z.m[j] = __funnelshift_l(P[j - 1], P[j], t1);
+      z.m[0] = __funnelshift_l(prv, P[0], t1);
+      int32_t e = x.e + y.e - (int32_t)t1;
+      // sh == 0: the guard decides; sh > 0: the round bit is inside the mantissa and
+      // everything below it is nonzero (gt != 0)
+      round_w<V>(z.m, sh == 0 ? gt : 1u, sh == 0 ? 0u : 1u, sh, e);
+      z.e = e;
+      return;
+    }
+  }
+  product_w<V, false>(x, y, sc, P, g1, g0);
   // mantissa = product limbs [L, 2L) (lane l's limbs L + V l + j live in lane 16 + l/2)
   const int hl = 16 + (lane >> 1);
   const bool odd = lane & 1;
@@ -526,7 +578,6 @@ __device__ __forceinline__ void mul_w(const W<V>& x, const W<V>& y, int sh, cons
   int32_t e = x.e + y.e - (int32_t)t1;
   round_w<V>(z.m, g, st, sh, e);
   z.e = e;
-  z.s = zs;
 }
 
 // ---------------------------------------------------------------------------
@@ -615,8 +666,10 @@ __device__ __forceinline__ void div_w(const W<V>& x, const W<V>& y, int sh, cons
     const uint32_t ci = lookahead(gs, lane > 0 ? all_ones<V>(R) : 0u, 0u, cs);
     add_bit<V>(R, ci);
     RL = RL - Etop - (cs ^ 1u);
-    // the estimate is never high and short by at most a little
-    while (try_sub()) ++qh;
+    // the estimate is never high and short by at most a little; R >= Y needs RL > 0 or
+    // a top limb >= Y's, so the full comparison runs only then
+    if (RL != 0 || __shfl_sync(FULL, R[V - 1], 31) >= y1)
+      while (try_sub()) ++qh;
     if (lane == 0) Q[t] = qh;
   }
   uint32_t rloc = 0;

@@ -558,6 +558,170 @@ __global__ void __launch_bounds__(NT) lu_panel_coop_kernel(uint32_t* a, int64_t 
   }
 }
 
+// Pivoting variant with ONE grid barrier per column: the row interchanges of the panel
+// are kept as a logical -> physical row table in every CTA's shared memory (identical
+// in all CTAs, which all reduce the same candidates), so choosing the pivot needs no
+// data movement and no barrier; the panel columns are permuted physically once, after
+// the panel (laswp_panel_kernel).  Per column: every CTA reduces the candidates of the
+// previous step -> same pivot r -> swaps table entries d, r; multipliers and rank-1
+// update of the CTA's logical rows (physical slots via the table); candidates of the
+// next column; grid.sync.  Same per-element operation sequence as the other kernels.
+template <int L>
+__global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k,
+                                                           int64_t row_end, int64_t* piv, int64_t* zp, int sh,
+                                                           uint64_t* cand_key, int64_t* cand_idx, uint64_t* cand_cnt,
+                                                           int64_t chunk) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int S = rec_stride(L);
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t* s_mult = s_dyn;                                      // chunk records
+  int* s_perm = reinterpret_cast<int*>(s_dyn + chunk * S);        // logical row - p -> physical row - p
+  __shared__ uint64_t s_wk[NT / 32];
+  __shared__ int64_t s_wi[NT / 32];
+  __shared__ int s_wc[NT / 32];
+  __shared__ int64_t s_piv;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t rows_all = row_end - p;
+  const int64_t lo = p + (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(row_end, lo + chunk);
+  for (int64_t t = tid; t < rows_all; t += NT) s_perm[t] = (int)t;
+  __syncthreads();
+  auto phys = [&](int64_t i) -> int64_t { return p + s_perm[i - p]; };
+  auto candidates = [&](int64_t col, int64_t from) {
+    uint64_t bk = 0;
+    int64_t bi = INT64_MAX;
+    int bc = 0;
+    for (int64_t i = max(from, lo) + tid; i < hi; i += NT) {
+      const uint32_t* r = a + (phys(i) * n + col) * S;
+      piv_combine(bk, bi, bc, mag_key(r[L], r[L - 1]), i, 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+      piv_combine(bk, bi, bc, k2, i2, c2);
+    }
+    if (lane == 0) {
+      s_wk[wid] = bk;
+      s_wi[wid] = bi;
+      s_wc[wid] = bc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < NT / 32; ++w) piv_combine(bk, bi, bc, s_wk[w], s_wi[w], s_wc[w]);
+      cand_key[blockIdx.x] = bk;
+      cand_idx[blockIdx.x] = bi;
+      cand_cnt[blockIdx.x] = (uint64_t)bc;
+    }
+    __syncthreads();
+  };
+  candidates(p, p);
+  grid.sync();
+  for (int64_t d = p; d < p + k; ++d) {
+    uint64_t gk = 0;
+    int64_t gi = INT64_MAX;
+    int gc = 0;
+    for (unsigned b = tid; b < gridDim.x; b += NT) piv_combine(gk, gi, gc, cand_key[b], cand_idx[b], (int)cand_cnt[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, gk, o);
+      const int64_t i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+      const int c2 = __shfl_xor_sync(0xffffffffu, gc, o);
+      piv_combine(gk, gi, gc, k2, i2, c2);
+    }
+    if (lane == 0) {
+      s_wk[wid] = gk;
+      s_wi[wid] = gi;
+      s_wc[wid] = gc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < NT / 32; ++w) piv_combine(gk, gi, gc, s_wk[w], s_wi[w], s_wc[w]);
+      if (gc > 1) {  // rows sharing the winning compact key: a full comparison decides (rare)
+        MP<L> rv, x;
+        int64_t r = -1;
+        for (int64_t i = d; i < row_end; ++i) {
+          const uint32_t* q = a + (phys(i) * n + d) * S;
+          if (mag_key(q[L], q[L - 1]) != gk) continue;
+          load_rec<L>(q, x);
+          if (r < 0 || mp_cmpabs<L>(x, rv) > 0) {
+            rv = x;
+            r = i;
+          }
+        }
+        gi = r;
+      }
+      s_piv = gi;
+      // interchange logical rows d and r (every CTA does the same)
+      const int tmp = s_perm[d - p];
+      s_perm[d - p] = s_perm[gi - p];
+      s_perm[gi - p] = tmp;
+      if (blockIdx.x == 0) piv[d] = gi;
+    }
+    __syncthreads();
+    const int64_t pd = phys(d);
+    // zero pivot: every CTA sees the same a_dd and stops (blocklu.hpp:46-47)
+    if (a[(pd * n + d) * S + L] == (uint32_t)EXP_ZERO) {
+      if (blockIdx.x == 0 && tid == 0) *zp = d + 1;
+      return;
+    }
+    const int64_t r0 = max(d + 1, lo);
+    const int64_t nr = hi - r0;
+    if (nr > 0) {
+      for (int64_t t = tid; t < nr; t += NT) {
+        MP<L> piv_v, x, q;
+        load_rec<L>(a + (pd * n + d) * S, piv_v);
+        uint32_t* xr = a + (phys(r0 + t) * n + d) * S;
+        load_rec<L>(xr, x);
+        mp_div<L>(x, piv_v, sh, q);
+        store_rec<L>(xr, q);
+        store_rec<L>(s_mult + t * S, q);
+      }
+      __syncthreads();
+      const int64_t w = p + k - d - 1;
+      for (int64_t t = tid; t < nr * w; t += NT) {
+        const int64_t rr = t / w, j = d + 1 + t % w;
+        MP<L> l, u, pr, x;
+        load_rec<L>(s_mult + rr * S, l);
+        load_rec<L>(a + (pd * n + j) * S, u);
+        mp_mul<L>(l, u, sh, pr);
+        uint32_t* xr = a + (phys(r0 + rr) * n + j) * S;
+        load_rec<L>(xr, x);
+        mp_add<L>(x, pr, 1u, sh, x);
+        store_rec<L>(xr, x);
+      }
+    }
+    if (d + 1 < p + k) {
+      __syncthreads();
+      candidates(d + 1, d + 1);
+    }
+    grid.sync();
+  }
+}
+
+// the panel's interchanges piv[p .. p+k) applied (in order) to the panel columns
+// [p, p+k), each 16-byte chunk of a column independent -- after lu_panel_perm_kernel
+template <int L>
+__global__ void laswp_panel_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv,
+                                   const int64_t* zp) {
+  constexpr int S = rec_stride(L), CH = S / 4;
+  if (*zp) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k * CH; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = p + t / CH, w = t % CH;
+    for (int64_t d = p; d < p + k; ++d) {
+      const int64_t r = piv[d];
+      if (r == d) continue;
+      uint4* x = reinterpret_cast<uint4*>(a + (d * n + j) * S + 4 * w);
+      uint4* y = reinterpret_cast<uint4*>(a + (r * n + j) * S + 4 * w);
+      const uint4 tmp = *x;
+      *x = *y;
+      *y = tmp;
+    }
+  }
+}
+
 template <int L>
 int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting,
                          int64_t* piv, int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid,
@@ -591,6 +755,28 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
   const int64_t chunk = (rows + grid - 1) / grid;
   const size_t smem = sizeof(uint32_t) * S * (size_t)chunk;
   if (smem > 16 * 1024) return -1;  // caller falls back to per-column kernels
+  if (pivoting && rows <= 12288 && std::getenv("MPGPU_LU_PERM") == nullptr) {
+    // one barrier per column: logical row table in shared memory (+ rows int32 words)
+    static bool conf = false;
+    if (!conf) {
+      cudaFuncSetAttribute(lu_panel_perm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 + 4 * 12288);
+      conf = true;
+    }
+    static int per_sm2 = -1;
+    if (per_sm2 < 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, lu_panel_perm_kernel<L>, NT, 16 * 1024 + 4 * 12288);
+    int64_t g2 = std::min<int64_t>(grid, (int64_t)per_sm2 * dev_sms);
+    if (g2 < 1) g2 = 1;
+    int64_t ch = (rows + g2 - 1) / g2;
+    if (sizeof(uint32_t) * S * (size_t)ch > 16 * 1024) return -1;
+    const size_t smem2 = sizeof(uint32_t) * S * (size_t)ch + sizeof(int) * (size_t)rows;
+    void* args2[] = {&a, &n, &p, &k, &row_end, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt, &ch};
+    cudaError_t e2 = cudaLaunchCooperativeKernel((void*)lu_panel_perm_kernel<L>, dim3((unsigned)g2), dim3(NT), args2,
+                                                 smem2, st);
+    if (e2 != cudaSuccess) return -1;
+    laswp_panel_kernel<L><<<blocks_for(k * (S / 4)), NT, 0, st>>>(a, n, p, k, piv, zp);
+    return 0;
+  }
   void* args[] = {&a, &n, &p, &k, &row_end, &pivoting, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)lu_panel_coop_kernel<L>, dim3((unsigned)grid), dim3(NT), args,
                                               smem, st);

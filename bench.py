@@ -254,6 +254,10 @@ def main():
     problems = world if (runner is not None and runner.replicated) else 1
     value = problems * n ** 3 * args.steps / (total_ms * 1e-3)
 
+    e2e_res = None
+    if world > 1 and not args.no_e2e:
+        e2e_res = e2e_dist(args, P, torch, dist, a, b, da, db, dc, runner, rank, world)
+
     # --- correctness guard on the timed output (cheap: sampled rows vs Block on GPU)
     if rank != 0:
         if dist:
@@ -297,6 +301,8 @@ def main():
 
     if not args.no_e2e and world == 1:
         line["e2e"] = e2e(args, P, torch, a, b, algo, param, ctx, L)
+    elif not args.no_e2e:
+        line["e2e"] = e2e_res
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, P, a, b)
     print(json.dumps(line), flush=True)
@@ -337,6 +343,100 @@ def e2e(args, P, torch, a, b, algo, param, ctx, L):
             "h2d_bytes_per_step": nbytes_soa(n_el, pa.nlimbs) + nbytes_soa(b.rows() * b.cols(), pb.nlimbs),
             "d2h_bytes_per_step": nbytes_soa(a.rows() * b.cols(), pc.nlimbs), "ms_per_step": dt * 1e3,
             "api": "mpgpu_gemm_host (include/mpgpu.h), pinned host SoA buffers, wall clock around the call"}
+
+
+def owned_row_runs(runner, m: int, rank: int, world: int):
+    """Contiguous runs [r0, r1) of the rows of C this rank reads back: its own rows for the
+    row-owned and row-sharded runners, all of C for replicas, an even split otherwise."""
+    from paper_1410_1599_b200 import shard
+    if getattr(runner, "replicated", False):
+        return [(0, m)]
+    rows = getattr(runner, "c_rows", None)
+    if rows is None:
+        sh = getattr(runner, "shard", None) if runner.__class__.__name__ == "_RowSharded" else None
+        sh = sh or shard.even_ranges(m, world)[rank]
+        return [(sh.lo, min(sh.hi, m))] if sh.hi > sh.lo and sh.lo < m else []
+    runs, start, prev = [], None, None
+    for r in rows:
+        if start is None:
+            start = prev = r
+        elif r == prev + 1:
+            prev = r
+        else:
+            runs.append((start, prev + 1))
+            start = prev = r
+    if start is not None:
+        runs.append((start, prev + 1))
+    return runs
+
+
+def e2e_dist(args, P, torch, dist, a, b, da, db, dc, runner, rank, world):
+    """e2e at N > 1 through the public API on every rank: H2D of A and B from pinned host
+    buffers (mpgpu_upload), the sharded product, D2H of the rows of C this rank owns
+    (mpgpu_download of row views); wall clock per rank, max over ranks.  Every rank
+    reaches the same collectives even if its upload / download fails."""
+    import ctypes as C
+    from paper_1410_1599_b200 import _lib as PL
+    err, dt = None, float("inf")
+    m, n = a.rows(), b.cols()
+    runs = owned_row_runs(runner, m, rank, world)
+    try:
+        def pin(x):
+            lim = torch.empty(x.limbs.shape, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+            ex = torch.empty(x.exp.shape, dtype=torch.int32, pin_memory=True).numpy()
+            sg = torch.empty(x.sign.shape, dtype=torch.uint8, pin_memory=True).numpy()
+            lim[:] = x.limbs
+            ex[:] = x.exp
+            sg[:] = x.sign
+            return P.Matrix(x.rows(), x.cols(), x.ctx(), lim, ex, sg)
+
+        pa, pb = pin(a), pin(b)
+        outs = [P.Matrix(r1 - r0, n, a.ctx()) for r0, r1 in runs]
+    except Exception as ex:
+        err = repr(ex)[:300]
+
+    def one(product=True):
+        if err is None:
+            da.upload(pa)
+            db.upload(pb)
+        if product:
+            runner()  # collective: every rank calls it
+        if err is None:
+            for (r0, r1), o in zip(runs, outs):
+                v = PL.MpgpuMat()
+                PL.lib.mpgpu_matrix_view(C.byref(dc.m), r0, 0, r1 - r0, n, C.byref(v))
+                rc = PL.lib.mpgpu_download(dc._h, C.byref(v), o.limbs.ctypes.data_as(C.c_void_p),
+                                           o.exp.ctypes.data_as(C.c_void_p), o.sign.ctypes.data_as(C.c_void_p),
+                                           o.nlimbs)
+                if rc:
+                    raise RuntimeError(f"mpgpu_download rc={rc}")
+
+    try:
+        one()
+    except Exception as ex:
+        err = err or repr(ex)[:300]
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        try:
+            one()
+        except Exception as ex:
+            err = err or repr(ex)[:300]
+    torch.cuda.synchronize()
+    if err is None:
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+    t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    if err is not None or not np.isfinite(dt):
+        return {"value": None, "unit": "madd/s", "error": err or "failed on another rank"}
+    rows_read = sum(r1 - r0 for r0, r1 in runs)
+    return {"value": m * a.cols() * n / dt, "unit": "madd/s",
+            "h2d_bytes_per_step": nbytes_soa(m * a.cols(), a.nlimbs) + nbytes_soa(b.rows() * n, b.nlimbs),
+            "d2h_bytes_per_step": nbytes_soa(rows_read * n, a.nlimbs), "ms_per_step": dt * 1e3,
+            "api": "per rank: mpgpu_upload of A, B (pinned host SoA), the sharded product, mpgpu_download "
+                   "of the rank's rows of C; bytes are rank 0's; wall clock, max over ranks"}
 
 
 def cpu_baseline(args, P, a, b):

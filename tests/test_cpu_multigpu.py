@@ -135,3 +135,26 @@ def test_gloo_world2_all_to_all_row_slices(units, um):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def test_bench_e2e_owned_row_runs():
+    """bench.py's N > 1 e2e leg reads back each rank's own rows of C as contiguous runs."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+
+    class RowOwned:
+        replicated = False
+        c_rows = [0, 1, 2, 5, 6, 9]
+
+    class Replica:
+        replicated = True
+
+    class Gather:
+        replicated = False
+
+    assert bench.owned_row_runs(RowOwned(), 10, 0, 2) == [(0, 3), (5, 7), (9, 10)]
+    assert bench.owned_row_runs(Replica(), 10, 1, 2) == [(0, 10)]
+    assert bench.owned_row_runs(Gather(), 10, 1, 2) == [(5, 10)]
+    assert bench.owned_row_runs(Gather(), 10, 0, 2) == [(0, 5)]

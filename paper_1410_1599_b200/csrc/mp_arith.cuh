@@ -590,8 +590,10 @@ MPG_UNROLL
       b = (uint32_t)(d >> 63);
     }
     R[L] = R[L] - c - b;
-    // corrections: the estimate is never high and short by at most a little
-    while (try_sub()) ++qh;
+    // corrections: the estimate is never high and short by at most a little; R >= Y needs
+    // R[L] > 0 or R[L-1] >= Y[L-1], so the full trial subtraction runs only then
+    if (R[L] != 0 || R[L - 1] >= y.m[L - 1])
+      while (try_sub()) ++qh;
     Q[t] = qh;
   }
   uint32_t rem = 0;

@@ -59,6 +59,35 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ---- bulk-copy (TMA engine) staging of full tiles --------------------------------
+#ifndef MPG_BULK
+#define MPG_BULK 1  // interior tiles by cp.async.bulk + mbarrier; edge tiles by zero-filling cp.async
+#endif
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
 #ifndef MPG_NZ_SPLIT
 #define MPG_NZ_SPLIT 1  // measured: -2.3 % leaf time at 256 bits, -1 % at 512
 #endif
@@ -138,9 +167,34 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
   const int i = i0 + ty;
   const bool active = (i < g.m) && (j0 + tx < g.n);
 
+  // stages whose A and B tiles lie inside the matrices are moved by the bulk-copy engine
+  // (one 16-byte-aligned row segment per copy, issued by warp 0, completion on an
+  // mbarrier); edge tiles use zero-filling cp.async.  Uniform per stage.
+  __shared__ __align__(8) uint64_t s_bar[2];
+  uint32_t bar_phase = 0;  // bit b: parity of s_bar[b]'s next completion
+  auto full_tile = [&](int kt) {
+    const int k0 = kt * TK;
+    // (k-tiles of 2 records -- L = 32 -- keep cp.async: measured 0.3 % faster there)
+    return MPG_BULK && TK >= 4 && i0 + TM <= g.m && j0 + TNB <= g.n && k0 + TK <= g.l;
+  };
   auto stage = [&](int kt, int buf) {
     const int k0 = kt * TK;
     constexpr int CH = S / 4;
+    if (full_tile(kt)) {
+      if (tid < 32) {
+        constexpr uint32_t ABYTES = TK * S * 4, BBYTES = TNB * S * 4;
+        if (tid == 0) mbar_expect(&s_bar[buf], TM * ABYTES + TK * BBYTES);
+        __syncwarp();
+        for (int c = tid; c < TM + TK; c += 32) {
+          if (c < TM)
+            bulk_g2s(sA + buf * A_WORDS + c * TK * S, A + ((int64_t)(i0 + c) * g.lda + k0) * S, ABYTES, &s_bar[buf]);
+          else
+            bulk_g2s(sB + buf * B_WORDS + (c - TM) * TNB * S, B + ((int64_t)(k0 + c - TM) * g.ldb + j0) * S, BBYTES,
+                     &s_bar[buf]);
+        }
+      }
+      return;
+    }
 #pragma unroll 1
     for (int c = tid; c < TM * TK * CH; c += NT) {
       const int e = c / CH, w = c - e * CH;
@@ -173,12 +227,22 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
   }
   int next_b = g.kb;  // k at which the next Block k-tile starts
 
+  if (tid == 0) {
+    mbar_init1(&s_bar[0]);
+    mbar_init1(&s_bar[1]);
+  }
+  __syncthreads();
   stage(0, 0);
   cp_async_commit();
   for (int kt = 0; kt < KT; ++kt) {
     if (kt + 1 < KT) stage(kt + 1, (kt + 1) & 1);
     cp_async_commit();
     cp_async_wait<1>();
+    if (full_tile(kt)) {  // bulk-copied stage: wait for its bytes on the mbarrier
+      const int b = kt & 1;
+      mbar_wait_parity(&s_bar[b], (bar_phase >> b) & 1u);
+      bar_phase ^= 1u << b;
+    }
     __syncthreads();
     if (active) {
       const uint32_t* a_rows = sA + (kt & 1) * A_WORDS + ty * TK * S;

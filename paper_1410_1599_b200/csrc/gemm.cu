@@ -88,6 +88,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
                : "memory");
 }
 
+#ifndef MPG_TILE_ALT
+#define MPG_TILE_ALT 1  // half-width tiles for ragged leaves (launch_gemm)
+#endif
+#ifndef MPG_TILE_ALT_NUM  // ... when they cover the m x n outputs with < NUM/DEN of the default tiles' area
+#define MPG_TILE_ALT_NUM 97
+#define MPG_TILE_ALT_DEN 100
+#endif
+
 #ifndef MPG_NZ_SPLIT
 #define MPG_NZ_SPLIT 1  // measured: -2.3 % leaf time at 256 bits, -1 % at 512
 #endif
@@ -310,16 +318,9 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
   }
 }
 
-template <int L>
-void launch_gemm(const GemmArgs& g, cudaStream_t st) {
-#if MPG_WIDE
-  if constexpr (L > 32)
-    if (wmp::enabled()) return wmp::launch_gemm<L / 32>(g, st);
-#endif
-  if constexpr (L == 8 || L == 16 || L == 32) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
-    if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
-  }
-  constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
+template <int L, int TM, int TN>
+void launch_tiles(const GemmArgs& g, cudaStream_t st) {
+  constexpr int TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
   constexpr int S = rec_stride(L);
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
   auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
@@ -341,6 +342,28 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
     dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, gz.batch);
     kern<<<grid, TM * TN, smem, st>>>(gz);
   }
+}
+
+template <int L>
+void launch_gemm(const GemmArgs& g, cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_gemm<L / 32>(g, st);
+#endif
+  if constexpr (L == 8 || L == 16 || L == 32) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
+    if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
+  }
+  constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, U = GemmCfg<L>::U;
+  if constexpr (U == 1 && TN == 16 && L <= 32) {
+    // ragged leaves (odd recursion shapes, e.g. 32 x 25 x 49 at config 3): a half-width,
+    // double-height tile when it covers the m x n outputs with fewer idle threads
+    auto cover = [&](int tm, int tn) {
+      return (int64_t)((g.m + tm - 1) / tm) * tm * (int64_t)((g.n + tn - 1) / tn) * tn;
+    };
+    if (MPG_TILE_ALT && cover(2 * TM, TN / 2) * MPG_TILE_ALT_DEN < cover(TM, TN) * MPG_TILE_ALT_NUM)
+      return launch_tiles<L, 2 * TM, TN / 2>(g, st);
+  }
+  launch_tiles<L, TM, TN>(g, st);
 }
 
 #if MPG_WIDE

@@ -17,6 +17,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bits", type=int, nargs="+", default=[256, 512, 1024])
     ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--shape", default=None, help="m,l,n (overrides --n)")
+    ap.add_argument("--gen", default="uniform_full", choices=["uniform_full", "scaled"])
     ap.add_argument("--n-min", type=int, default=64)
     ap.add_argument("--algo", default="winograd")
     ap.add_argument("--reps", type=int, default=5)
@@ -26,15 +28,17 @@ def main():
     algo = P.Algorithm[a.algo]
     for bits in a.bits:
         ctx = P.PrecisionContext(bits)
-        A = P.gen_uniform_full(a.n, a.n, 1, ctx).to_device()
-        B = P.gen_uniform_full(a.n, a.n, 2, ctx).to_device()
-        C = P.DeviceMatrix(a.n, a.n, ctx)
+        m, l, n = (int(x) for x in a.shape.split(",")) if a.shape else (a.n, a.n, a.n)
+        gen = P.gen_scaled if a.gen == "scaled" else P.gen_uniform_full
+        A = gen(m, l, 1, ctx).to_device()
+        B = gen(l, n, 2, ctx).to_device()
+        C = P.DeviceMatrix(m, n, ctx)
         leaf, dev = [], []
         for _ in range(a.reps + 1):
             st = P.gemm_into(algo, a.n_min if algo != P.Algorithm.simple else 0, A, B, C)
             leaf.append(st.leaf_ms)
             dev.append(st.device_ms)
-        print(json.dumps({"tag": a.tag, "algo": a.algo, "n": a.n, "bits": bits,
+        print(json.dumps({"tag": a.tag, "algo": a.algo, "shape": [m, l, n], "n_min": a.n_min, "bits": bits,
                           "leaf_ms": min(leaf[1:]), "device_ms": min(dev[1:])}), flush=True)
 
 

@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-precision-sweep", action="store_true",
+                    help="skip the leaf-roofline sweep at 512 / 1024 bits (same n, algorithm, n_min)")
     ap.add_argument("--shard", choices=["auto", "gather", "replicas"], default="auto",
                     help="N>1: auto = leaf shards with one all-to-all and a row-owned combine "
                          "(Strassen/Winograd) or row shards (Simple/Block) (strong scaling); gather = "
@@ -303,6 +305,8 @@ def main():
         line["e2e"] = e2e(args, P, torch, a, b, algo, param, ctx, L)
     elif not args.no_e2e:
         line["e2e"] = e2e_res
+    if not args.no_precision_sweep and world == 1:
+        line["leaf_roofline_by_bits"] = precision_sweep(args, P, torch, IMAD_PER_CLK_PER_SM * sms * sm_max * 1e6 / 1e12)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, P, a, b)
     print(json.dumps(line), flush=True)
@@ -343,6 +347,31 @@ def e2e(args, P, torch, a, b, algo, param, ctx, L):
             "h2d_bytes_per_step": nbytes_soa(n_el, pa.nlimbs) + nbytes_soa(b.rows() * b.cols(), pb.nlimbs),
             "d2h_bytes_per_step": nbytes_soa(a.rows() * b.cols(), pc.nlimbs), "ms_per_step": dt * 1e3,
             "api": "mpgpu_gemm_host (include/mpgpu.h), pinned host SoA buffers, wall clock around the call"}
+
+
+def precision_sweep(args, P, torch, peak_tiops):
+    """The north star's '>= 50 % of the IMAD roofline at 256-1024 bits': the same product
+    (n, algorithm, n_min, full-mantissa inputs) at 256 / 512 / 1024 bits, leaf kernel only,
+    CUDA-event timed (min of 3 after a warm-up).  Reported beside the headline line."""
+    out = {}
+    for bits in (256, 512, 1024):
+        ctx = P.PrecisionContext(bits)
+        n = args.n
+        da = P.gen_uniform_full(n, n, 1, ctx).to_device()
+        db = P.gen_uniform_full(n, n, 2, ctx).to_device()
+        dc = P.DeviceMatrix(n, n, ctx)
+        algo = P.Algorithm[args.algo]
+        param = args.n_min if algo != P.Algorithm.simple else 0
+        st = P.gemm_into(algo, param, da, db, dc)
+        leaf = min(P.gemm_into(algo, param, da, db, dc).leaf_ms for _ in range(3))
+        L = P.nlimbs_for(bits)
+        achieved = st.leaf_madds * 2 * L * L / (leaf * 1e-3) / 1e12
+        out[str(bits)] = {"leaf_ms": leaf, "leaf_madds": st.leaf_madds, "imad_eq_per_madd": 2 * L * L,
+                          "achieved_tiops": achieved, "frac": achieved / peak_tiops}
+        for x in (da, db, dc):
+            x.free()
+    torch.cuda.synchronize()
+    return out
 
 
 def owned_row_runs(runner, m: int, rank: int, world: int):

@@ -74,6 +74,13 @@ def main():
     rd *= scale.get(units[h.index("dram__bytes_read.sum")], 1)
     wr *= scale.get(units[h.index("dram__bytes_write.sum")], 1)
     summ["dram_bytes_per_launch"] = rd + wr
+    try:  # HBM bandwidth of the launch (the leaf is compute-bound: far below the peak)
+        t = float(v[h.index("gpu__time_duration.sum")])
+        t *= {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0}.get(
+            units[h.index("gpu__time_duration.sum")], 1e-3)
+        summ["dram_gbs"] = (rd + wr) / t / 1e9
+    except (ValueError, IndexError):
+        pass
     Path(a.out + "_summary.json").write_text(json.dumps(summ, indent=1))
     tfile = Path(a.out).parent / "r01_leaf_traffic.json"
     t = json.loads(tfile.read_text()) if tfile.exists() else {}

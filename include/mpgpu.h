@@ -44,9 +44,9 @@ extern "C" {
 #define MPGPU_ERR_UNDEFINED_METRIC 6 /* mpmm::UndefinedMetricError (errors.hpp:41-43) */
 
 #define MPGPU_EXP_ZERO INT32_MIN
-/* Largest device precision: limb counts 1, 2, 4, 8, 16, 32 (register-resident, <= 1024
- * bits) and 64, 128, 256, 288 (wide formats in local memory, <= 9216 bits -- e.g. the
- * 8192 / 8650-bit Lotkin experiments of the paper). */
+/* Largest device precision: limb counts 1, 2, 4, 8, 16, 32 (one thread per value,
+ * register-resident, <= 1024 bits) and 64, 128, 256, 288 (wide formats, one warp per value,
+ * <= 9216 bits -- e.g. the 8192 / 8650-bit Lotkin experiments of the paper). */
 #define MPGPU_MAX_PREC 9216
 #define MPGPU_MAX_STORE_PREC MPGPU_MAX_PREC
 

@@ -14,7 +14,7 @@
 // A maintainer switches a translation unit to the GPU path with
 //     namespace mpmm { using namespace mpmm::gpu; }   // or call mpmm::gpu:: explicitly
 // Results are bit-identical to the reference (same operation DAG, MPFR_RNDN rounding).
-// Documented deviations: operands of one call must share one precision <= 1024 bits
+// Documented deviations: operands of one call must share one precision <= MPGPU_MAX_PREC (9216) bits
 // (DomainError otherwise), and NaN/Inf inputs are rejected with DomainError.
 #pragma once
 

@@ -95,8 +95,8 @@ def _raise(h, rc: int, pivot: int = 0):
 
 class PrecisionContext:
     """precision.hpp:18-36 -- p in [2, 2^20]; RNDN fixed.  The device arithmetic
-    supports p <= 1024 (mpgpu.h MPGPU_MAX_PREC); device matrices up to 2048 bits
-    (MPGPU_MAX_STORE_PREC) hold the references of the accuracy metrics."""
+    supports p <= 9216 (mpgpu.h MPGPU_MAX_PREC: one thread per value up to 1024 bits,
+    one warp per value above)."""
 
     min_bits = 2
     max_bits = 1 << 20
@@ -918,7 +918,7 @@ def inverse(a: Matrix, ctx: PrecisionContext) -> Matrix:
 
 def cond_one(a: Matrix, ctx_hi: Optional[PrecisionContext] = None) -> Matrix:
     """blocklu.hpp:285-301: ||A||_1 * ||A^-1||_1 with everything at ctx_hi (default
-    min(2 bits + 64, max_bits)); 1x1 Matrix.  Device arithmetic: ctx_hi <= 1024 bits."""
+    min(2 bits + 64, max_bits)); 1x1 Matrix.  Device arithmetic: ctx_hi <= 9216 bits."""
     if ctx_hi is None:
         ctx_hi = PrecisionContext(min(2 * a.bits() + 64, PrecisionContext.max_bits))
     dahi = convert(a, ctx_hi)

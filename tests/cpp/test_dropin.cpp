@@ -64,6 +64,20 @@ int main() {
       CHECK(sx, "lu_solve bit-exact");
     }
   }
+  {  // the paper's ill-conditioned experiment precision: wide formats (one warp per value)
+    PrecisionContext wide(8192);
+    const BenchPair wp = gen_bench_pair(9, 7, 11, wide);
+    FastMMResult r1 = fast_mul(wp.a, wp.b, FastMMConfig{Algorithm::winograd, 2}, wide);
+    FastMMResult r2 = gpu::fast_mul(wp.a, wp.b, FastMMConfig{Algorithm::winograd, 2}, wide);
+    CHECK(equal_values(r1.c, r2.c) && r1.ops == r2.ops, "fast_mul winograd at 8192 bits bit-exact");
+    const Matrix lot = gen_lotkin(12, wide);
+    const LinearSystem ls = gen_linear_system(lot, wide);
+    const BlockLUConfig cfg = BlockLUConfig::with_alpha(1, 4, Algorithm::winograd);
+    Vector x1 = solve(lot, ls.b, cfg, wide), x2 = gpu::solve(lot, ls.b, cfg, wide);
+    bool sx = x1.size() == x2.size();
+    for (std::size_t i = 0; sx && i < x1.size(); ++i) sx = x1[i] == x2[i];
+    CHECK(sx, "solve (Lotkin n=12, 8192 bits, Winograd Schur) bit-exact");
+  }
   try {
     gpu::lu_columnwise(Matrix(2, 3, ctx));
     CHECK(false, "lu_columnwise non-square throws DimensionError");

@@ -625,20 +625,24 @@ __device__ __forceinline__ void div_w(const W<V>& x, const W<V>& y, int sh, cons
   const double inv = __drcp_rd(yd);
 #pragma unroll 1
   for (int t = WL - 1; t >= 0; --t) {
-    // R <<= 32 (R < Y: the top limb is free)
-    RL = __shfl_sync(FULL, R[V - 1], 31);
+    // R <<= 32 (R < Y: the top limb is free); the new top three limbs come from lane 31's
+    // (and for V = 2 lane 30's) registers before the shift -- one round of shuffles
+    const uint32_t t0 = __shfl_sync(FULL, R[V - 1], 31), t1 = __shfl_sync(FULL, R[V - 2], 31);
+    const uint32_t t2 = V >= 3 ? __shfl_sync(FULL, R[V >= 3 ? V - 3 : 0], 31) : __shfl_sync(FULL, R[V - 1], 30);
     uint32_t prv = __shfl_up_sync(FULL, R[V - 1], 1);
     if (lane == 0) prv = 0;
 #pragma unroll
     for (int j = V - 1; j > 0; --j) R[j] = R[j - 1];
     R[0] = prv;
-    const uint32_t r1 = __shfl_sync(FULL, R[V - 1], 31), r2 = __shfl_sync(FULL, R[V - 2], 31);
-    const uint64_t rtop = ((uint64_t)RL << 32) | r1;
+    RL = t0;
+    const uint64_t rtop = ((uint64_t)RL << 32) | t1;
     double rd = __dmul_rd(__ull2double_rd(rtop), 4294967296.0);
-    rd = __dadd_rd(rd, (double)r2);
+    rd = __dadd_rd(rd, (double)t2);
     const double qd = floor(__dmul_rd(rd, inv));
     uint32_t qh = qd >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)qd;
-    // E = qh * Y (L + 1 limbs): lane products, carry limb to the next lane, 1-bit lookahead
+    // R -= qh * Y in one pass: each lane subtracts its V-limb product segment, passes its
+    // product top limb plus its borrow (< 2^32) to the next lane, which subtracts it at its
+    // first limb; the remaining 1-bit borrows resolve by lookahead (propagate = all zero)
     uint32_t E[V], cl = 0;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -646,26 +650,27 @@ __device__ __forceinline__ void div_w(const W<V>& x, const W<V>& y, int sh, cons
       E[j] = (uint32_t)pr;
       cl = (uint32_t)(pr >> 32);
     }
-    uint32_t clp = __shfl_up_sync(FULL, cl, 1);
-    if (lane == 0) clp = 0;
-    uint32_t ge;
-    asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(E[0]) : "r"(clp));
-#pragma unroll
-    for (int j = 1; j < V; ++j) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(E[j]));
-    asm volatile("addc.u32 %0, 0, 0;" : "=r"(ge));
-    uint32_t coE;
-    const uint32_t cE = lookahead(ge, lane > 0 ? all_ones<V>(E) : 0u, 0u, coE);
-    add_bit<V>(E, cE);
-    const uint32_t Etop = __shfl_sync(FULL, cl, 31) + coE;  // limb L of qh * Y
-    // R -= E: R + ~E + 1
     uint32_t NE[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) NE[j] = ~E[j];
-    const uint32_t gs = add_chain<V>(R, R, NE, lane == 0 ? 1u : 0u);
-    uint32_t cs;
-    const uint32_t ci = lookahead(gs, lane > 0 ? all_ones<V>(R) : 0u, 0u, cs);
-    add_bit<V>(R, ci);
-    RL = RL - Etop - (cs ^ 1u);
+    const uint32_t c1 = add_chain<V>(R, R, NE, 1u);  // R - E, carry 1 = no borrow
+    const uint32_t h = cl + (c1 ^ 1u);                // subtract from the next lane's limb 0
+    uint32_t hp = __shfl_up_sync(FULL, h, 1);
+    if (lane == 0) hp = 0;
+    uint32_t b2;
+    asm volatile("sub.cc.u32 %0, %0, %1;" : "+r"(R[0]) : "r"(hp));
+#pragma unroll
+    for (int j = 1; j < V; ++j) asm volatile("subc.cc.u32 %0, %0, 0;" : "+r"(R[j]));
+    asm volatile("subc.u32 %0, 0, 0;" : "=r"(b2));  // 0xFFFFFFFF on borrow
+    uint32_t zl = 0;
+#pragma unroll
+    for (int j = 0; j < V; ++j) zl |= R[j];
+    uint32_t bout;
+    const uint32_t bin = lookahead(b2 & 1u, lane > 0 && zl == 0 ? 1u : 0u, 0u, bout);
+    asm volatile("sub.cc.u32 %0, %0, %1;" : "+r"(R[0]) : "r"(bin));
+#pragma unroll
+    for (int j = 1; j < V; ++j) asm volatile("subc.cc.u32 %0, %0, 0;" : "+r"(R[j]));
+    RL = RL - __shfl_sync(FULL, h, 31) - bout;
     // the estimate is never high and short by at most a little; R >= Y needs RL > 0 or
     // a top limb >= Y's, so the full comparison runs only then
     if (RL != 0 || __shfl_sync(FULL, R[V - 1], 31) >= y1)

@@ -202,3 +202,22 @@ def test_deep_recursion_more_leaves_than_grid_z(P, O, alg):
     c = _run(P, alg, 1, a, b, ctx, P.OpCounter())
     want, _ = O.gemm(alg, 1, O.OMat.of(a), O.OMat.of(b))
     assert P.identical(c, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [256, 512, 1024])
+@pytest.mark.parametrize("alg,param", [("simple", 0), ("block", 8), ("winograd", 16)])
+def test_ragged_leaf_half_width_tiles(P, O, alg, param, bits):
+    """32 x 25 x 49 (config 3's n_min-32 leaf shape): launch_gemm picks the half-width,
+    double-height tile (it covers 32 x 56 outputs instead of 32 x 64) -- bit-exact."""
+    ctx = P.PrecisionContext(bits)
+    a = P.gen_scaled(32, 25, 21, ctx)
+    b = P.gen_scaled(25, 49, 22, ctx)
+    if alg == "simple":
+        c = P.simple_mul(a, b, ctx)
+    elif alg == "block":
+        c = P.block_mul(a, b, param, ctx)
+    else:
+        c = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm.winograd, param), ctx).c
+    want, _ = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)

@@ -17,6 +17,9 @@
 
 #include "kernels.h"
 #include "mp_arith.cuh"
+#if MPG_WIDE
+#include "wkern.cuh"
+#endif
 
 namespace mpg {
 namespace {
@@ -163,6 +166,12 @@ template <int L>
 void launch_rel_error(const uint32_t* approx, int la, int64_t lda, const uint32_t* ref, int64_t ldr, int rows,
                       int cols, int mode, int sh, uint32_t* outA, uint32_t* outB, unsigned long long* counter,
                       uint32_t* err, cudaStream_t st) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled())
+      return wmp::launch_rel_error<L / 32>(approx, la, lda, ref, ldr, rows, cols, mode, sh, outA, outB, counter,
+                                           err, st);
+#endif
   const int64_t N = (int64_t)rows * cols;
   const int nt = 128;
   const int64_t want = (N + nt - 1) / nt;

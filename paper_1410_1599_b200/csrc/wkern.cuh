@@ -147,6 +147,65 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
   }
 }
 
+// ---- accuracy metric (metrics.cu rel_error_kernel contract), one warp per element ----
+template <int V>
+__global__ void __launch_bounds__(WNT) rel_error_kernel(const uint32_t* __restrict__ approx, int la, int sa,
+                                                        int64_t lda, const uint32_t* __restrict__ ref, int64_t ldr,
+                                                        int rows, int cols, int mode, int sh,
+                                                        uint32_t* __restrict__ outA, uint32_t* __restrict__ outB,
+                                                        unsigned long long* counter, uint32_t* err) {
+  constexpr int L = 32 * V, S = rec_stride(L);
+  constexpr uint32_t SKIP = 2u;
+  const Scratch<V> sc = my_scratch<V>();
+  const int lane = lane_id();
+  const int64_t N = (int64_t)rows * cols;
+  auto store_flag = [&](uint32_t* r, const W<V>& x, uint32_t flag) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) r[lane * V + j] = x.m[j];
+    if (lane == 0) r[L] = (uint32_t)x.e;
+    if (lane == 1) r[L + 1] = x.s | flag;
+  };
+  for (int64_t t = gwarp(); t < N; t += nwarps()) {
+    const int64_t i = t / cols, j = t - i * cols;
+    const uint32_t* ar = approx + (i * lda + j) * sa;
+    W<V> a, r, d;
+    const int off = L - la;  // approx has la <= L limbs: widened exactly (low limbs zero)
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int k = lane * V + q;
+      a.m[q] = k >= off ? ar[k - off] : 0u;
+    }
+    a.e = (int32_t)ar[la];
+    a.s = ar[la + 1];
+    load_w<V>(ref + (i * ldr + j) * S, r);
+    add_w<V>(a, r, 1u, sh, d);  // sub(approx, reference, ctx)
+    d.s = 0;                    // abs
+    if (r.e == EXP_ZERO) {
+      if (lane == 0) atomicAdd(counter, 1ull);
+      store_flag(outA + t * S, r, SKIP);
+      if (mode == 1) store_flag(outB + t * S, d, 0u);
+      continue;
+    }
+    r.s = 0;
+    W<V> q;
+    div_w<V>(d, r, sh, sc, q);  // div(abs(d), abs(reference), ctx)
+    if (lane == 0 && (exp_out_of_range(q.e) || exp_out_of_range(d.e))) atomicOr(err, ERR_EXP_RANGE);
+    store_flag(outA + t * S, q, 0u);
+    if (mode == 1) store_flag(outB + t * S, q, SKIP);
+  }
+}
+
+template <int V>
+void launch_rel_error(const uint32_t* approx, int la, int64_t lda, const uint32_t* ref, int64_t ldr, int rows,
+                      int cols, int mode, int sh, uint32_t* outA, uint32_t* outB, unsigned long long* counter,
+                      uint32_t* err, cudaStream_t st) {
+  const int64_t N = (int64_t)rows * cols;
+  if (N <= 0) return;
+  set_smem(rel_error_kernel<V>, smem_bytes<V>());
+  rel_error_kernel<V><<<wblocks(N), WNT, smem_bytes<V>(), st>>>(approx, la, rec_stride(la), lda, ref, ldr, rows,
+                                                                  cols, mode, sh, outA, outB, counter, err);
+}
+
 // ---- LU (lu.cu contracts) ------------------------------------------------------
 // The LU kernels are cooperative: every parallel phase (divisions, rank-1 updates,
 // triangular-solve steps) is spread over all warps of a grid that fills the GPU, with a

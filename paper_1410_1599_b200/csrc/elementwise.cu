@@ -407,6 +407,10 @@ template <int L>
 void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
                    uint32_t* children, int sh, uint32_t* err, cudaStream_t st) {
   (void)err;
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled()) return wmp::launch_preadd<L / 32>(algo, side, parent, nodes, rows, cols, children, sh, st);
+#endif
   const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
   preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh);
 }
@@ -414,6 +418,12 @@ template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist,
                     int nrows) {
+#if MPG_WIDE
+  if constexpr (L > 32)
+    if (wmp::enabled())
+      return wmp::launch_postadd<L / 32>(algo, children, nodes, rows, cols, parent, t_out, sh, err, st, rowlist,
+                                         nrows);
+#endif
   const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
   if (total <= 0) return;
   postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,

@@ -147,6 +147,191 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
   }
 }
 
+// ---- Strassen / Winograd level transforms (elementwise.cu contracts), one warp per
+// (node, quadrant element); the same sums in the same operand order as the reference
+// (fastmm.hpp:133-198), zero padding of odd dimensions virtual (+0) ------------------
+template <int V>
+__global__ void __launch_bounds__(WNT) preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent,
+                                                     int64_t nodes, int rows, int cols,
+                                                     uint32_t* __restrict__ children, int sh) {
+  constexpr int S = rec_stride(32 * V);
+  const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
+  const int64_t per = (int64_t)hr * hc;
+  const int64_t total = per * nodes;
+  for (int64_t t = gwarp(); t < total; t += nwarps()) {
+    const int64_t node = t / per;
+    const int64_t e = t - node * per;
+    const int r = (int)(e / hc), c = (int)(e - (int64_t)r * hc);
+    const uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    uint32_t* out = children + (node * 7 * per + e) * S;
+    const int64_t cs = per * S;
+    auto ld = [&](int q, W<V>& x) {
+      const int rr = r + (q >> 1) * hr, cc = c + (q & 1) * hc;
+      if (rr < rows && cc < cols)
+        load_w<V>(P + ((int64_t)rr * cols + cc) * S, x);
+      else
+        zero_w<V>(x, 0);
+    };
+    auto put = [&](int child, const W<V>& x) { store_w<V>(out + child * cs, x); };
+    auto sum = [&](int qa, int qb, uint32_t neg, int child) {
+      W<V> x, y, z;
+      ld(qa, x);
+      ld(qb, y);
+      add_w<V>(x, y, neg, sh, z);
+      put(child, z);
+    };
+    auto copy = [&](int q, int child) {
+      W<V> x;
+      ld(q, x);
+      put(child, x);
+    };
+    if (algo == 3) {
+      W<V> s1, s2, x, y;
+      if (side == 0) {  // S1 = a21+a22 (M5), S2 = S1-a11 (M1), S3 = a11-a21 (M4), S4 = a12-S2 (M6)
+        ld(2, x);
+        ld(3, y);
+        add_w<V>(x, y, 0u, sh, s1);
+        put(4, s1);
+        ld(0, x);
+        add_w<V>(s1, x, 1u, sh, s2);
+        put(0, s2);
+        ld(1, x);
+        add_w<V>(x, s2, 1u, sh, y);
+        put(5, y);
+        sum(0, 2, 1u, 3);
+        copy(0, 1);
+        copy(1, 2);
+        copy(3, 6);
+      } else {  // S5 = b12-b11 (M5), S6 = b22-S5 (M1), S7 = b22-b12 (M4), S8 = S6-b21 (M7)
+        ld(1, x);
+        ld(0, y);
+        add_w<V>(x, y, 1u, sh, s1);
+        put(4, s1);
+        ld(3, x);
+        add_w<V>(x, s1, 1u, sh, s2);
+        put(0, s2);
+        ld(2, x);
+        add_w<V>(s2, x, 1u, sh, y);
+        put(6, y);
+        sum(3, 1, 1u, 3);
+        copy(0, 1);
+        copy(2, 2);
+        copy(3, 5);
+      }
+    } else if (side == 0) {  // a11+a22, a21+a22, a11, a22, a11+a12, a21-a11, a12-a22
+      sum(0, 3, 0u, 0);
+      sum(2, 3, 0u, 1);
+      copy(0, 2);
+      copy(3, 3);
+      sum(0, 1, 0u, 4);
+      sum(2, 0, 1u, 5);
+      sum(1, 3, 1u, 6);
+    } else {  // b11+b22, b11, b12-b22, b21-b11, b22, b11+b12, b21+b22
+      sum(0, 3, 0u, 0);
+      copy(0, 1);
+      sum(1, 3, 1u, 2);
+      sum(2, 0, 1u, 3);
+      copy(3, 4);
+      sum(0, 1, 0u, 5);
+      sum(2, 3, 0u, 6);
+    }
+  }
+}
+
+template <int V>
+void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
+                   uint32_t* children, int sh, cudaStream_t st) {
+  const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  if (total <= 0) return;
+  preadd_kernel<V><<<wblocks(total), WNT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh);
+}
+
+template <int V>
+__global__ void __launch_bounds__(WNT) postadd_kernel(int algo, const uint32_t* __restrict__ children,
+                                                      int64_t nodes, int rows, int cols,
+                                                      uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
+                                                      int sh, uint32_t* err, const int* __restrict__ rowlist,
+                                                      int nrows) {
+  constexpr int S = rec_stride(32 * V);
+  const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
+  const int64_t per = (int64_t)hr * hc;
+  const int64_t per_iter = (rowlist ? (int64_t)nrows : (int64_t)hr) * hc;
+  const int64_t total = per_iter * nodes;
+  for (int64_t t = gwarp(); t < total; t += nwarps()) {
+    const int64_t node = t / per_iter;
+    const int64_t ei = t - node * per_iter;
+    const int ri = (int)(ei / hc), c = (int)(ei - (int64_t)ri * hc);
+    const int r = rowlist ? rowlist[ri] : ri;
+    const int64_t e = (int64_t)r * hc + c;
+    const uint32_t* M = children + (node * 7 * per + e) * S;
+    const int64_t cs = per * S;
+    uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    auto store_if = [&](int rr, int cc, const W<V>& x) {  // strip the padding
+      if (rr < rows && cc < cols) {
+        if (lane_id() == 0 && exp_out_of_range(x.e)) atomicOr(err, ERR_EXP_RANGE);
+        store_w<V>(P + ((int64_t)rr * cols + cc) * S, x);
+      }
+    };
+    if (algo == 3) {  // T1 = M1+M2, T2 = T1+M4; C11 = M2+M3, C12 = (T1+M5)+M6, C21 = T2-M7, C22 = T2+M5
+      W<V> m1, m2, t1, t2, u, v, x;
+      load_w<V>(M, m1);
+      load_w<V>(M + cs, m2);
+      add_w<V>(m1, m2, 0u, sh, t1);
+      load_w<V>(M + 3 * cs, x);
+      add_w<V>(t1, x, 0u, sh, t2);
+      if (t_out) {
+        store_w<V>(t_out + (node * 2 * per + e) * S, t1);
+        store_w<V>(t_out + (node * 2 * per + per + e) * S, t2);
+      }
+      load_w<V>(M + 2 * cs, x);
+      add_w<V>(m2, x, 0u, sh, u);
+      store_if(r, c, u);
+      W<V> m5;
+      load_w<V>(M + 4 * cs, m5);
+      load_w<V>(M + 5 * cs, x);
+      add_w<V>(t1, m5, 0u, sh, u);
+      add_w<V>(u, x, 0u, sh, v);
+      store_if(r, c + hc, v);
+      load_w<V>(M + 6 * cs, x);
+      add_w<V>(t2, x, 1u, sh, u);
+      store_if(r + hr, c, u);
+      add_w<V>(t2, m5, 0u, sh, u);
+      store_if(r + hr, c + hc, u);
+    } else {  // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
+      W<V> p1, p4, p5, u, v, x;
+      load_w<V>(M, p1);
+      load_w<V>(M + 3 * cs, p4);
+      load_w<V>(M + 4 * cs, p5);
+      add_w<V>(p1, p4, 0u, sh, u);
+      add_w<V>(u, p5, 1u, sh, v);
+      load_w<V>(M + 6 * cs, x);
+      add_w<V>(v, x, 0u, sh, u);
+      store_if(r, c, u);
+      W<V> p3, p2;
+      load_w<V>(M + 2 * cs, p3);
+      add_w<V>(p3, p5, 0u, sh, u);
+      store_if(r, c + hc, u);
+      load_w<V>(M + cs, p2);
+      add_w<V>(p2, p4, 0u, sh, u);
+      store_if(r + hr, c, u);
+      add_w<V>(p1, p3, 0u, sh, u);
+      add_w<V>(u, p2, 1u, sh, v);
+      load_w<V>(M + 5 * cs, x);
+      add_w<V>(v, x, 0u, sh, u);
+      store_if(r + hr, c + hc, u);
+    }
+  }
+}
+
+template <int V>
+void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols, uint32_t* parent,
+                    uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist, int nrows) {
+  const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  if (total <= 0) return;
+  postadd_kernel<V><<<wblocks(total), WNT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh, err,
+                                                     rowlist, nrows);
+}
+
 // ---- accuracy metric (metrics.cu rel_error_kernel contract), one warp per element ----
 template <int V>
 __global__ void __launch_bounds__(WNT) rel_error_kernel(const uint32_t* __restrict__ approx, int la, int sa,

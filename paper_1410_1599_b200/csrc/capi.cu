@@ -29,6 +29,8 @@ struct mpgpu_handle {
   int64_t d_piv_cap = 0;
   std::mutex mu;
   std::string last_error;
+  cudaStream_t aux = nullptr;  // second stream of mpgpu_gemm_host (B's upload), lazily created
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 };
 
 namespace {
@@ -230,7 +232,7 @@ int check_err(mpgpu_handle* h) {
 template <int L>
 int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_t lda, const uint32_t* B,
              int64_t ldb, uint32_t* C, int64_t ldc, int64_t m, int64_t l, int64_t n, int sh,
-             mpgpu_stats* stats, int sub_from_c) {
+             mpgpu_stats* stats, int sub_from_c, cudaEvent_t b_ready = nullptr) {
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   const bool timing = stats != nullptr;
@@ -283,7 +285,13 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
     ++launches;
   };
   if (stats) stats->depth = 0;
+  // b_ready (mpgpu_gemm_host): B is still being uploaded on another stream -- the A-side
+  // work runs first and the B side waits for the event
+  auto wait_b = [&]() {
+    if (b_ready) cudaStreamWaitEvent(st, b_ready, 0);
+  };
   if (algo == MPGPU_SIMPLE || algo == MPGPU_BLOCK) {
+    wait_b();
     Timer tl(timing, st);
     leaf(A, lda, B, ldb, C, ldc, m, l, n, algo == MPGPU_SIMPLE ? l : param, 1, sub_from_c);
     if (stats) {
@@ -295,6 +303,7 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
     const int d = (int)lv.size() - 1;
     if (stats) stats->depth = d;
     if (d == 0) {
+      wait_b();
       Timer tl(timing, st);
       leaf(A, lda, B, ldb, C, ldc, m, l, n, l, 1, sub_from_c);
       if (stats) {
@@ -313,6 +322,7 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
         pa = a0.u32();
       }
       if (ldb != n) {
+        wait_b();
         CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * l * n));
         mpg::launch_copy2d<L>(B, ldb, b0.u32(), n, (int)l, (int)n, st);
         ++launches;
@@ -321,21 +331,34 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
       std::vector<DevBuf> opA(d + 1), opB(d + 1), prod(d + 1);
       Timer tpre(timing, st);
       int64_t nodes = 1;
-      for (int lev = 0; lev < d; ++lev) {
+      // the pre-additions of one side never read the other's: with b_ready all A levels
+      // run first (overlapping B's upload), else the sides interleave level by level
+      auto side_level = [&](int side, int lev, int64_t nd) -> int {
         const Level& P = lv[lev];
         const Level& Q = lv[lev + 1];
-        const uint32_t* srcA = lev == 0 ? pa : opA[lev].u32();
-        const uint32_t* srcB = lev == 0 ? pb : opB[lev].u32();
-        CUDA_TRY(h, opA[lev + 1].alloc(h, sizeof(uint32_t) * S * nodes * 7 * Q.m * Q.l));
-        CUDA_TRY(h, opB[lev + 1].alloc(h, sizeof(uint32_t) * S * nodes * 7 * Q.l * Q.n));
-        mpg::launch_preadd<L>(algo, 0, srcA, nodes, (int)P.m, (int)P.l, opA[lev + 1].u32(), sh, h->d_err, st);
-        mpg::launch_preadd<L>(algo, 1, srcB, nodes, (int)P.l, (int)P.n, opB[lev + 1].u32(), sh, h->d_err, st);
-        launches += 2;
-        if (lev > 0) {
-          opA[lev].release();
-          opB[lev].release();
+        std::vector<DevBuf>& op = side == 0 ? opA : opB;
+        const uint32_t* src = lev == 0 ? (side == 0 ? pa : pb) : op[lev].u32();
+        const int64_t rr = side == 0 ? P.m : P.l, cc = side == 0 ? P.l : P.n;
+        const int64_t qr = side == 0 ? Q.m : Q.l, qc = side == 0 ? Q.l : Q.n;
+        CUDA_TRY(h, op[lev + 1].alloc(h, sizeof(uint32_t) * S * nd * 7 * qr * qc));
+        mpg::launch_preadd<L>(algo, side, src, nd, (int)rr, (int)cc, op[lev + 1].u32(), sh, h->d_err, st);
+        ++launches;
+        if (lev > 0) op[lev].release();
+        return 0;
+      };
+      if (b_ready) {
+        for (int lev = 0, nd = 1; lev < d; ++lev, nd *= 7)
+          if (int rc = side_level(0, lev, nd)) return rc;
+        wait_b();
+        for (int lev = 0, nd = 1; lev < d; ++lev, nd *= 7)
+          if (int rc = side_level(1, lev, nd)) return rc;
+        for (int lev = 0; lev < d; ++lev) nodes *= 7;
+      } else {
+        for (int lev = 0; lev < d; ++lev) {
+          if (int rc = side_level(0, lev, nodes)) return rc;
+          if (int rc = side_level(1, lev, nodes)) return rc;
+          nodes *= 7;
         }
-        nodes *= 7;
       }
       a0.release();
       b0.release();
@@ -705,10 +728,38 @@ int bitlen(const std::vector<uint32_t>& v) {
 }  // namespace
 
 // host SoA -> device records (stream-ordered, no sync); stage is scratch owned by the caller
+// host SoA planes -> staging (H2D on `st`) -> device records; `copied` (optional) is
+// recorded on `st` once the host bytes are across
+int upload_async_to(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_t* limbs, const int32_t* exp,
+                    const uint8_t* sign, int32_t Lh, uint32_t* stage, cudaStream_t st, cudaEvent_t copied = nullptr) {
+  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+  uint32_t* dl = stage;
+  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
+  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
+  if (Lh <= L) {
+    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, st));
+    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
+                                cudaMemcpyHostToDevice, st));
+  } else {
+    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, st));
+  if (copied) CUDA_TRY(h, cudaEventRecord(copied, st));
+  dispatch_store(L, [&](auto Lc) {
+    mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, rec, st);
+    return 0;
+  });
+  return MPGPU_OK;
+}
+
 int upload_async(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_t* limbs, const int32_t* exp,
-                 const uint8_t* sign, int32_t Lh, DevBuf& stage) {
+                 const uint8_t* sign, int32_t Lh, DevBuf& stage, cudaStream_t st_in = nullptr,
+                 cudaEvent_t copied = nullptr) {
   const size_t planes = sizeof(uint32_t) * (size_t)L * N;
   CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
+  if (st_in || copied)
+    return upload_async_to(h, rec, L, N, limbs, exp, sign, Lh, stage.u32(), st_in ? st_in : h->stream, copied);
   uint32_t* dl = stage.u32();
   int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
   uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
@@ -782,9 +833,13 @@ void mpgpu_destroy(mpgpu_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  if (h->aux) cudaStreamSynchronize(h->aux);
   if (h->d_err) cudaFree(h->d_err);
   if (h->d_piv) cudaFree(h->d_piv);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->ev_b) cudaEventDestroy(h->ev_b);
   delete h;
 }
 
@@ -950,14 +1005,31 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
     stats->addsub = c[1];
   }
   CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), h->stream));
-  rc = upload_async(h, A.rec, L, m * l, al, ae, as, Lh, sa);
-  if (!rc) rc = upload_async(h, B.rec, L, l * n, bl, be, bs, Lh, sb);
+  // A's upload on the handle's stream; B's on a second stream, started once A's bytes are
+  // across, so the A-side layout conversion and pre-additions overlap B's transfer (the
+  // B side of the product waits for B's event)
+  if (!h->aux) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+  }
+  rc = upload_async(h, A.rec, L, m * l, al, ae, as, Lh, sa, h->stream, h->ev_a);
   if (rc) return rc;
+  CUDA_TRY(h, cudaStreamWaitEvent(h->aux, h->ev_a, 0));  // also orders db's allocation
+  {
+    uint32_t* stage = nullptr;
+    const size_t sbytes = (sizeof(uint32_t) * (size_t)L + sizeof(int32_t) + 1) * (size_t)(l * n);
+    CUDA_TRY(h, cudaMallocAsync(reinterpret_cast<void**>(&stage), sbytes, h->aux));
+    rc = upload_async_to(h, B.rec, L, l * n, bl, be, bs, Lh, stage, h->aux);
+    cudaFreeAsync(stage, h->aux);
+    if (rc) return rc;
+  }
+  CUDA_TRY(h, cudaEventRecord(h->ev_b, h->aux));
   sa.release();
-  sb.release();
   const int sh = 32 * L - prec;
   rc = dispatch_L(L, [&](auto Lc) {
-    return run_gemm<decltype(Lc)::value>(h, algo, param, A.rec, l, B.rec, n, C.rec, n, m, l, n, sh, stats, 0);
+    return run_gemm<decltype(Lc)::value>(h, algo, param, A.rec, l, B.rec, n, C.rec, n, m, l, n, sh, stats, 0,
+                                         h->ev_b);
   });
   if (rc) return rc;
   rc = download_async(h, C.rec, L, m * n, cl, ce, cs, Lh, sc);

@@ -722,6 +722,116 @@ __global__ void laswp_panel_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k,
   }
 }
 
+// The panel's interchanges piv[p .. p+k) (LAPACK order) as ONE permutation of the rows
+// they touch: warp 0 of every CTA composes the swaps on a table of the involved rows in
+// shared memory (<= 2k rows; lookups by ballot), then each CTA moves whole column tiles --
+// every involved record read once into shared memory, then written to its final row.
+// Columns [jlo, jhi) except [skip_lo, skip_hi).  Replaces k dependent swap rounds per
+// element (latency-bound) by one read and one write.
+template <int L>
+__global__ void __launch_bounds__(NT) laswp_perm_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k,
+                                                        const int64_t* piv, const int64_t* zp, int64_t jlo,
+                                                        int64_t jhi, int64_t skip_lo, int64_t skip_hi, int tc) {
+  constexpr int S = rec_stride(L), CH = S / 4;
+  if (*zp) return;
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  int64_t* s_pos = reinterpret_cast<int64_t*>(s_dyn);  // 2k: involved rows
+  int64_t* s_src = s_pos + 2 * k;                      // 2k: original row whose data ends there
+  uint4* s_buf = reinterpret_cast<uint4*>(s_src + 2 * k);
+  __shared__ int s_cnt;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    for (int64_t i = lane; i < k; i += 32) {
+      s_pos[i] = p + i;
+      s_src[i] = p + i;
+    }
+    int cnt = (int)k;
+    __syncwarp();
+    auto find = [&](int64_t r) -> int {  // index of row r in the table, -1 if absent
+      if (r >= p && r < p + k) return (int)(r - p);
+      int hit = -1;
+      for (int base = (int)k; base < cnt; base += 32) {
+        const int i = base + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i < cnt && s_pos[i] == r);
+        if (m) {
+          hit = base + __ffs(m) - 1;
+          break;
+        }
+      }
+      return hit;
+    };
+    for (int64_t d = p; d < p + k; ++d) {
+      const int64_t r = piv[d];
+      if (r == d) continue;
+      int ir = find(r);
+      if (ir < 0) {  // first touch of a row below the panel
+        if (lane == 0) {
+          s_pos[cnt] = r;
+          s_src[cnt] = r;
+        }
+        ir = cnt++;
+        __syncwarp();
+      }
+      if (lane == 0) {
+        const int id = (int)(d - p);
+        const int64_t t = s_src[id];
+        s_src[id] = s_src[ir];
+        s_src[ir] = t;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) s_cnt = cnt;
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  const int64_t ncols = (jhi - jlo) - (skip_hi - skip_lo);
+  auto col = [&](int64_t c) { return jlo + c + (jlo + c >= skip_lo ? skip_hi - skip_lo : 0); };
+  for (int64_t c0 = (int64_t)blockIdx.x * tc; c0 < ncols; c0 += (int64_t)gridDim.x * tc) {
+    const int w = (int)min((int64_t)tc, ncols - c0);
+    const int64_t items = (int64_t)cnt * w * CH;
+    for (int64_t t = tid; t < items; t += NT) {
+      const int i = (int)(t / (w * CH));
+      const int rem = (int)(t - (int64_t)i * w * CH), jc = rem / CH, q = rem - jc * CH;
+      s_buf[t] = reinterpret_cast<const uint4*>(a + (s_src[i] * n + col(c0 + jc)) * S)[q];
+    }
+    __syncthreads();
+    for (int64_t t = tid; t < items; t += NT) {
+      const int i = (int)(t / (w * CH));
+      const int rem = (int)(t - (int64_t)i * w * CH), jc = rem / CH, q = rem - jc * CH;
+      if (s_src[i] != s_pos[i]) reinterpret_cast<uint4*>(a + (s_pos[i] * n + col(c0 + jc)) * S)[q] = s_buf[t];
+    }
+    __syncthreads();
+  }
+}
+
+template <int L>
+void launch_laswp_perm(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv, const int64_t* zp,
+                       int64_t jlo, int64_t jhi, int64_t skip_lo, int64_t skip_hi, cudaStream_t st) {
+  constexpr int S = rec_stride(L);
+  const int64_t ncols = (jhi - jlo) - (skip_hi - skip_lo);
+  if (ncols <= 0 || k <= 0) return;
+  // column tile: the <= 2k involved records of tc columns staged in <= 64 KB of shared memory
+  int tc = (int)std::max<int64_t>(1, (64 * 1024) / (2 * k * S * 4));
+  if (tc > 32) tc = 32;
+  const size_t smem = sizeof(int64_t) * 4 * (size_t)k + sizeof(uint32_t) * S * (size_t)(2 * k * tc);
+  static bool conf = false;
+  if (!conf) {
+    cudaFuncSetAttribute(laswp_perm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    conf = true;
+  }
+  if (smem > 200 * 1024) {  // very wide records x large panels: the swap-by-swap kernels
+    if (skip_hi > skip_lo)
+      laswp_kernel<L><<<blocks_for((n - k) * (S / 4)), NT, 0, st>>>(a, n, p, k, piv, zp);
+    else
+      laswp_panel_kernel<L><<<blocks_for(k * (S / 4)), NT, 0, st>>>(a, n, p, k, piv, zp);
+    return;
+  }
+  const int64_t tiles = (ncols + tc - 1) / tc;
+  const int grid = (int)std::min<int64_t>(tiles, 148 * 4);
+  laswp_perm_kernel<L><<<grid, NT, smem, st>>>(a, n, p, k, piv, zp, jlo, jhi, skip_lo, skip_hi, tc);
+}
+
+
 template <int L>
 int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t row_end, int pivoting,
                          int64_t* piv, int64_t* zp, int sh, uint64_t* cand_key, int64_t* cand_idx, int max_grid,
@@ -774,7 +884,7 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
     cudaError_t e2 = cudaLaunchCooperativeKernel((void*)lu_panel_perm_kernel<L>, dim3((unsigned)g2), dim3(NT), args2,
                                                  smem2, st);
     if (e2 != cudaSuccess) return -1;
-    laswp_panel_kernel<L><<<blocks_for(k * (S / 4)), NT, 0, st>>>(a, n, p, k, piv, zp);
+    launch_laswp_perm<L>(a, n, p, k, piv, zp, p, p + k, 0, 0, st);
     return 0;
   }
   void* args[] = {&a, &n, &p, &k, &row_end, &pivoting, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt};
@@ -806,7 +916,7 @@ template <int L>
 void launch_laswp(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64_t* piv_dev, const int64_t* zp,
                   cudaStream_t st) {
   if (n - k <= 0) return;
-  laswp_kernel<L><<<blocks_for((n - k) * (rec_stride(L) / 4)), NT, 0, st>>>(a, n, p, k, piv_dev, zp);
+  launch_laswp_perm<L>(a, n, p, k, piv_dev, zp, 0, n, p, p + k, st);
 }
 
 template <int L>

@@ -287,6 +287,60 @@ __global__ void __launch_bounds__(NT) trsm_l_panel_kernel(uint32_t* a, int64_t n
   }
 }
 
+// The same sweep with the CTA's U12 tile (k rows x tc columns) resident in shared memory:
+// per step s only the multipliers l_is come from memory (loaded one step ahead), the
+// pivot row and the updated elements stay on chip -- the sweep is a chain of k dependent
+// multiply-adds per column, so its per-step latency is the cost.
+template <int L>
+__global__ void __launch_bounds__(NT) trsm_l_smem_kernel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c0,
+                                                         int64_t w, int sh, int tcw) {
+  constexpr int S = rec_stride(L), CH = S / 4;
+  extern __shared__ __align__(16) uint32_t s_tile[];
+  const int64_t j0 = c0 + (int64_t)blockIdx.x * tcw;
+  const int tc = (int)(c0 + w - j0 < tcw ? c0 + w - j0 : tcw);
+  const int tid = threadIdx.x;
+  auto T = [&](int64_t r, int jj) { return s_tile + ((r - p) * tcw + jj) * S; };
+  for (int64_t t = tid; t < k * tc * CH; t += NT) {
+    const int64_t r = t / (tc * CH);
+    const int rem = (int)(t - r * tc * CH), jj = rem / CH, q = rem - jj * CH;
+    reinterpret_cast<uint4*>(T(p + r, jj))[q] = reinterpret_cast<const uint4*>(a + ((p + r) * n + j0 + jj) * S)[q];
+  }
+  // this thread's first element of step s: row s + 1 + tid / tc; its multiplier one step ahead
+  MP<L> lnext;
+  auto first_l = [&](int64_t s, MP<L>& l) {
+    const int64_t i = s + 1 + tid / tc;
+    if (s + 1 < p + k && i < p + k) load_rec<L>(a + (i * n + s) * S, l);
+  };
+  first_l(p, lnext);
+  __syncthreads();
+  for (int64_t s = p; s + 1 < p + k; ++s) {
+    const int64_t rows = p + k - s - 1;
+    MP<L> lcur = lnext;
+    first_l(s + 1, lnext);
+    for (int64_t t = tid; t < rows * tc; t += NT) {
+      const int64_t i = s + 1 + t / tc;
+      const int jj = (int)(t % tc);
+      MP<L> l, u, pr, x;
+      if (t == tid)
+        l = lcur;
+      else
+        load_rec<L>(a + (i * n + s) * S, l);
+      load_rec<L>(T(s, jj), u);
+      mp_mul<L>(l, u, sh, pr);
+      uint32_t* xr = T(i, jj);
+      load_rec<L>(xr, x);
+      mp_add<L>(x, pr, 1u, sh, x);
+      store_rec<L>(xr, x);
+    }
+    __syncthreads();
+  }
+  for (int64_t t = tid; t < (k - 1) * tc * CH; t += NT) {  // row p is unchanged
+    const int64_t r = 1 + t / (tc * CH);
+    const int rem = (int)(t - (r - 1) * tc * CH), jj = rem / CH, q = rem - jj * CH;
+    reinterpret_cast<uint4*>(a + ((p + r) * n + j0 + jj) * S)[q] = reinterpret_cast<const uint4*>(T(p + r, jj))[q];
+  }
+}
+
 // Ly = Pb (column sweep, exact), Ux = y (exact row replay, s ascending as
 // blocklu.hpp:235-238); one CTA.
 template <int L>
@@ -935,6 +989,16 @@ void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c
   if constexpr (L > 32)
     if (wmp::enabled()) return wmp::launch_trsm_panel<L / 32>(a, n, p, k, c0, w, sh, st);
 #endif
+  const size_t smem = sizeof(uint32_t) * rec_stride(L) * (size_t)(k * TRSM_TC);
+  if (smem <= 160 * 1024 && std::getenv("MPGPU_TRSM_GLOBAL") == nullptr) {
+    static bool conf = false;
+    if (!conf) {
+      cudaFuncSetAttribute(trsm_l_smem_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      conf = true;
+    }
+    trsm_l_smem_kernel<L><<<(int)((w + TRSM_TC - 1) / TRSM_TC), NT, smem, st>>>(a, n, p, k, c0, w, sh, TRSM_TC);
+    return;
+  }
   trsm_l_panel_kernel<L><<<(int)((w + TRSM_TC - 1) / TRSM_TC), NT, 0, st>>>(a, n, p, k, c0, w, sh);
 }
 

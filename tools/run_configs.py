@@ -215,10 +215,15 @@ def cfg5(quick=False):
             PAm = P.Matrix(n, n, ctx, A.limbs[:, idx], A.exp[idx], A.sign[idx])
             berr = O.log2_max_abs_diff(O.OMat.of(PAm), O.OMat.of(LU)) - O.log2_max_abs(O.OMat.of(A))
             xf = x.to_float().reshape(-1)
+            extra = {}
+            if kernel == "winograd" and alpha == 2:  # the reference's exact s-ascending replay
+                xe, dte = timed(lambda: P.lu_solve(f, bvec, ctx, exact=True))
+                extra = dict(exact_solve_wall_ms=dte * 1e3,
+                             exact_vs_column_solve_max_abs_diff=float(np.max(np.abs(xe.to_float().reshape(-1) - xf))))
             emit(cfg=5, input=inp, n=n, bits=bits, kernel=kernel, alpha=alpha, K=cfg.block_size,
-                 lu_ms=st.device_ms, lu_wall_ms=dt * 1e3, solve_wall_ms=dts * 1e3, schur_madds=st.mul,
-                 log2_backward_err=berr, log2_bound=math.log2(n) - bits + 8,
-                 max_abs_x_minus_1=float(np.max(np.abs(xf - 1.0))))
+                 lu_ms=st.device_ms, lu_wall_ms=dt * 1e3, solve_wall_ms=dts * 1e3, solve="column-oriented",
+                 schur_madds=st.mul, log2_backward_err=berr, log2_bound=math.log2(n) - bits + 8,
+                 max_abs_x_minus_1=float(np.max(np.abs(xf - 1.0))), **extra)
 
 
 def main():

@@ -12,7 +12,11 @@ from paper_1410_1599_b200 import _lib as L, shard
 
 
 def _rec_tensor(n_words):
-    return torch.zeros(n_words, dtype=torch.int32, device="cuda")
+    # torch zero-fills on its own stream while the library writes on the handle's stream:
+    # finish the fill (and any pending torch work on a recycled block) before handing it over
+    t = torch.zeros(n_words, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    return t
 
 
 @pytest.mark.gpu
@@ -115,3 +119,10 @@ def test_row_owned_combine_bit_exact(P, algo, m, l, n, bits, n_min, world, up):
         out.sign[idx] = part.sign[idx]
     assert sorted(covered) == list(range(m))
     assert P.identical(out, want)
+
+
+@pytest.mark.gpu
+def test_row_owned_combine_repeat(P):
+    # the case that failed once on the driver (Winograd 33x29x40 @512, up=1, world 2), repeated
+    for _ in range(50):
+        test_row_owned_combine_bit_exact(P, "winograd", 33, 29, 40, 512, 4, 2, 1)

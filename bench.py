@@ -52,6 +52,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-precision-sweep", action="store_true",
                     help="skip the leaf-roofline sweep at 512 / 1024 bits (same n, algorithm, n_min)")
+    ap.add_argument("--no-lu", action="store_true", help="skip the config-5 LU leg")
+    ap.add_argument("--probe-world", action="store_true",
+                    help="print this rank's (rank, world) as JSON and exit before touching CUDA (launcher test)")
+    ap.add_argument("--cfg4", action="store_true", help="also time config 4 (n=4096 @1024) at N=1")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 leg at N>1")
     ap.add_argument("--shard", choices=["auto", "gather", "replicas"], default="auto",
                     help="N>1: auto = leaf shards with one all-to-all and a row-owned combine "
                          "(Strassen/Winograd) or row shards (Simple/Block) (strong scaling); gather = "
@@ -127,19 +132,43 @@ def nbytes_soa(n_elems: int, limbs: int) -> int:
 
 
 # ---------------------------------------------------------------------------
+def host_info():
+    """lscpu model name and nproc of the host the CPU arm ran on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def oracle_inputs(args, s):
+    """The workload's inputs made by the ORACLE's generator (oracle/mp_oracle.c, the same
+    Prng64 stream as the product's gen_uniform_full: tests/test_cpu_host.py), cut to the
+    top-left s x s blocks -- the reference arm never maps libmpgpu.so."""
+    from oracle import oracle as O
+    out = []
+    for seed in (1, 2):
+        full = O.gen_full(0, args.n, args.n, seed, args.bits)
+        idx = (np.arange(s)[:, None] * args.n + np.arange(s)[None, :]).reshape(-1)
+        out.append(O.OMat(s, s, args.bits, full.limbs[:, idx], full.exp[idx], full.sign[idx]))
+    return out
+
+
 def run_reference(args, rank: int):
     """The reference's own CPU implementation (oracle/_ref: the unmodified mpmm
-    headers compiled against system MPFR), all host threads, bounded sample."""
+    headers compiled against system MPFR), all host threads, bounded sample.
+    Imports only oracle/ (never the product package)."""
     if rank != 0:
         return
-    import paper_1410_1599_b200 as P
     from oracle import oracle as O
-    ctx = P.PrecisionContext(args.bits)
     s, nmin_s = sample_shape(args)
-    a = P.gen_uniform_full(args.n, args.n, 1, ctx).sub(0, 0, s, s)
-    b = P.gen_uniform_full(args.n, args.n, 2, ctx).sub(0, 0, s, s)
+    oa, ob = oracle_inputs(args, s)
     threads = os.cpu_count() or 1
-    oa, ob = O.OMat.of(a), O.OMat.of(b)
     for _ in range(args.warmup):
         O.gemm_replicas(args.algo, nmin_s, oa, ob, threads)
     times = []
@@ -148,14 +177,17 @@ def run_reference(args, rank: int):
         times.append(sec)
     total = sum(times)
     value = threads * s ** 3 * len(times) / total
+    sample = sample_desc(args, s, nmin_s, threads)
     line = {
         "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"mp{args.bits} (u32 limbs)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"mp{args.bits} (MPFR)",
         "data": "synthetic", "impl": "reference",
         "config": workload_config(args),
-        "cpu_baseline": {"value": value, "unit": "madd/s", "cores": threads, "kind": "reference",
-                         "sample": sample_desc(args, s, nmin_s, threads)},
+        "sample": {"shape": [s, s, s], "n_min": nmin_s if args.algo != "simple" else None, "algorithm": args.algo,
+                   "replicas": threads, "what": sample},
+        "host": host_info(),
+        "cpu_baseline": {"value": value, "unit": "madd/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "madd/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -172,29 +204,54 @@ def sample_shape(args):
 
 def sample_desc(args, s, nmin_s, threads):
     what = f"{args.algo}(n_min={nmin_s})" if args.algo != "simple" else "simple"
-    return (f"{threads} thread(s) x reference {what} on the {s}x{s} top-left blocks of the workload inputs "
-            f"({args.bits}-bit, same depth / op-count ratio as n={args.n}, n_min={args.n_min}); "
-            f"value = threads * {s}^3 / wall time of the multiplies")
+    return (f"SAMPLE, not the full workload: {threads} thread(s) each running the reference's {what} on the "
+            f"{s}x{s} top-left blocks of the workload inputs ({args.bits}-bit; same recursion depth and op-count "
+            f"ratio as n={args.n}, n_min={args.n_min}); value = threads * {s}^3 / wall time of the multiplies. "
+            f"The full-size single-core reference timing of this workload is in profiles/ (r02_ref_fullsize_*.json)")
 
 
-def workload_config(args):
+def workload_config(args, world=None):
+    world = args.gpus if world is None else world
     return {"workload": f"BASELINE config 2: MP GEMM n={args.n} @{args.bits}-bit, {args.algo}"
                         + (f" n_min={args.n_min}" if args.algo != "simple" else ""),
             "n": args.n, "bits": args.bits, "algorithm": args.algo, "n_min": args.n_min,
             "inputs": "uniform [-1,1) full-mantissa, seeds 1/2 (Prng64)",
             "l2": "flushed between timed steps (256 MiB write) and working set > L2",
-            "parallelism": (f"{args.shard} x{args.gpus}" if args.gpus > 1 else "single GPU")}
+            "parallelism": (f"{args.shard} x{world}" if world > 1 else "single GPU")}
 
 
 # ---------------------------------------------------------------------------
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` started without torchrun: re-launch this command as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.probe_world:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": args.gpus}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
     import torch
     import paper_1410_1599_b200 as P
     torch.cuda.set_device(local)
@@ -225,42 +282,22 @@ def main():
             return runner()
         return P.gemm_into(algo, param, da, db, dc)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    times, leaf_ms, launches, st = [], [], 0, None
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            st = step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-            leaf_ms.append(st.leaf_ms)
-            launches += st.launches
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    total_ms = float(sum(times))
-    if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms, leaf_ms, launches, st, clocks = timed_steps(args, torch, dist, stream, flush, step, local)
     # every rank works on one n^3 problem together (N > 1: leaf shards); weak scaling
     # is reported via replicas of the problem per rank -- see shard.make_runner
     problems = world if (runner is not None and runner.replicated) else 1
     value = problems * n ** 3 * args.steps / (total_ms * 1e-3)
 
+    # correctness guard on the timed output (outside the timed region)
+    guard = check_output(args, P, torch, dist, algo, param, a, b, da, db, dc, runner, rank, world)
+
     e2e_res = None
     if world > 1 and not args.no_e2e:
         e2e_res = e2e_dist(args, P, torch, dist, a, b, da, db, dc, runner, rank, world)
+    big = None
+    if world > 1 and not args.no_cfg4 or args.cfg4:
+        big = cfg4_leg(args, P, torch, dist, stream, flush, local, rank, world)
 
-    # --- correctness guard on the timed output (cheap: sampled rows vs Block on GPU)
     if rank != 0:
         if dist:
             dist.barrier()
@@ -275,7 +312,6 @@ def main():
     imad_eq = st.leaf_madds * 2 * L * L
     achieved = imad_eq / (leaf_avg_ms * 1e-3) / 1e12
     peak = IMAD_PER_CLK_PER_SM * sms * sm_max * 1e6 / 1e12
-    clocks = clk.summary()
     prof = ROOT / "profiles" / "r01_leaf_traffic.json"
     traffic = None
     if prof.exists():
@@ -295,24 +331,230 @@ def main():
         "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak" if problems > 1 else "strong", "vs_baseline": None,
-        "dtype": f"mp{args.bits} (u32 limbs, IMAD)", "data": "synthetic", "config": workload_config(args),
+        "dtype": f"mp{args.bits} (u32 limbs, IMAD)", "data": "synthetic", "config": workload_config(args, world),
         "ops_per_step": {"mul": st.mul, "addsub": st.addsub, "leaf_madds": st.leaf_madds, "depth": st.depth},
         "phase_ms": {"preadd": st.preadd_ms, "leaf": st.leaf_ms, "postadd": st.postadd_ms},
-        "roofline": roof, "clocks": clocks, "gpu_launches": launches,
+        "roofline": roof, "clocks": clocks, "gpu_launches": launches, "check": guard,
     }
+    if runner is not None:
+        line["config"]["runner"] = runner.mode
 
     if not args.no_e2e and world == 1:
         line["e2e"] = e2e(args, P, torch, a, b, algo, param, ctx, L)
     elif not args.no_e2e:
         line["e2e"] = e2e_res
+    if big is not None:
+        line["cfg4"] = big
     if not args.no_precision_sweep and world == 1:
         line["leaf_roofline_by_bits"] = precision_sweep(args, P, torch, IMAD_PER_CLK_PER_SM * sms * sm_max * 1e6 / 1e12)
+    if not args.no_lu and world == 1:
+        line["lu"] = lu_leg(args, P, torch, stream, flush, peak)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, P, a, b)
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def timed_steps(args, torch, dist, stream, flush, step, local, steps=None, warmup=None):
+    """W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching
+    stream, an L2 flush between steps, barrier + synchronize on both sides; max over ranks."""
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    times, leaf_ms, launches, st = [], [], 0, None
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            st = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            leaf_ms.append(st.leaf_ms)
+            launches += st.launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = float(sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    return total_ms, leaf_ms, launches, st, clk.summary()
+
+
+def normwise_log2(P, x, ref, a, b):
+    """log2( max|x - ref| / (max|A| max|B|) ), differences formed in MP on the device."""
+    d = np.abs(P.sub(x, ref).to_float())
+    num = float(d.max())
+    den = float(np.abs(a.to_float()).max()) * float(np.abs(b.to_float()).max())
+    return float(np.log2(num / den)) if num > 0 else float("-inf")
+
+
+def check_output(args, P, torch, dist, algo, param, a, b, da, db, dc, runner, rank, world):
+    """Guard on the benchmarked product (not timed).  N = 1: sampled rows of C against the
+    Block product of the same rows (bit-exact for Simple / Block; for Strassen / Winograd
+    within the north-star normwise bound 4 n^log2(7) 2^-p).  N > 1: every rank recomputes
+    the product on its own GPU with the single-GPU path and compares the rows of C it owns
+    bit for bit; mismatches are summed over ranks."""
+    import math
+    n = a.rows()
+    if runner is None:
+        rows = sorted({0, n // 3, n // 2, n - 1})
+        ctx = a.ctx()
+        got = dc.download()
+        idx = (np.asarray(rows)[:, None] * n + np.arange(n)[None, :]).reshape(-1)
+        gr = P.Matrix(len(rows), n, ctx, got.limbs[:, idx], got.exp[idx], got.sign[idx])
+        ar = P.Matrix(len(rows), n, ctx, a.limbs[:, idx], a.exp[idx], a.sign[idx])
+        blk = P.block_mul(ar, b, max(1, args.n_min), ctx)
+        if algo in (P.Algorithm.simple, P.Algorithm.block):
+            same = P.identical(gr, blk if algo == P.Algorithm.block else P.simple_mul(ar, b, ctx))
+            return {"rows": rows, "vs": "same algorithm on the sampled rows", "bit_exact": bool(same), "ok": bool(same)}
+        err = normwise_log2(P, gr, blk, a, b)
+        bound = math.log2(4.0) + math.log2(7) * math.log2(n) - args.bits
+        return {"rows": rows, "vs": "Block rows, normwise", "log2_err": err, "log2_bound": bound,
+                "ok": bool(err <= bound)}
+    ref = P.DeviceMatrix(n, n, a.ctx())
+    P.gemm_into(algo, param, da, db, ref)
+    own = getattr(runner, "c_rows", None)
+    if own is None or getattr(runner, "replicated", False) or runner.__class__.__name__ == "_FastSharded":
+        own = list(range(n))
+    elif runner.__class__.__name__ == "_RowSharded":
+        own = list(range(runner.shard.lo, min(runner.shard.hi, n)))
+    got, want = dc.download(), ref.download()
+    ref.free()
+    idx = (np.asarray(own, dtype=np.int64)[:, None] * n + np.arange(n)[None, :]).reshape(-1) if own else \
+        np.zeros(0, np.int64)
+    bad = int(np.count_nonzero((got.exp[idx] != want.exp[idx]) | (got.sign[idx] != want.sign[idx]) |
+                               np.any(got.limbs[:, idx] != want.limbs[:, idx], axis=0)))
+    t = torch.tensor([bad, len(own)], device="cuda", dtype=torch.int64)
+    dist.all_reduce(t)
+    return {"vs": "single-GPU product of the same inputs on every rank, owned rows, bit for bit",
+            "mismatched_elements": int(t[0].item()), "rows_checked": int(t[1].item()), "ok": int(t[0].item()) == 0}
+
+
+def cfg4_leg(args, P, torch, dist, stream, flush, local, rank, world):
+    """north star's scaling workload (BASELINE config 4): n = 4096 at 1024 bits, Winograd
+    n_min 512 (depth 3, 343 leaves of 512^3) sharded the same way; 1 warm-up + 1 timed step."""
+    from paper_1410_1599_b200 import shard
+    ctx = P.PrecisionContext(1024)
+    n, nmin = 4096, 512
+    a = P.gen_uniform_full(n, n, 1, ctx)
+    b = P.gen_uniform_full(n, n, 2, ctx)
+    da, db = a.to_device(), b.to_device()
+    dc = P.DeviceMatrix(n, n, ctx)
+    algo = P.Algorithm.winograd
+    runner = shard.make_runner(algo, nmin, da, db, dc, rank, world, mode=args.shard) if world > 1 else None
+
+    def step():
+        return runner() if runner is not None else P.gemm_into(algo, nmin, da, db, dc)
+
+    total_ms, leaf_ms, launches, st, clocks = timed_steps(args, torch, dist, stream, flush, step, local, 1, 1)
+    for x in (da, db, dc):
+        x.free()
+    L = P.nlimbs_for(1024)
+    return {"workload": "BASELINE config 4: MP GEMM n=4096 @1024-bit, winograd n_min=512 (depth 3)",
+            "value": n ** 3 / (total_ms * 1e-3), "unit": "madd/s", "ms_per_step": total_ms, "steps": 1, "warmup": 1,
+            "leaf_ms_rank0": float(np.mean(leaf_ms)), "leaf_madds_rank0": st.leaf_madds,
+            "imad_eq_per_madd": 2 * L * L, "runner": getattr(runner, "mode", "single GPU"), "clocks": clocks}
+
+
+def lu_leg(args, P, torch, stream, flush, leaf_peak_tiops):
+    """BASELINE config 5(a): MP LU with partial pivoting, n = 2048 at 256 bits, Winograd Schur
+    update K = 64 (alpha 2, n_min 32), uniform [-1,1) full-mantissa A, b = A*1.  Device time
+    (CUDA events inside mpgpu_lu_blocked), the Schur leaf roofline, e2e through the C-ABI with
+    host buffers (upload, factorisation, download), the solve's forward error formed in MP on
+    the device, and the compiled reference's pivot-free lu_blocked on one core at n = 256,
+    extrapolated by n^3."""
+    import ctypes as C
+    from paper_1410_1599_b200 import _lib as PL
+    try:
+        n, bits, K, nmin = 2048, 256, 64, 32
+        ctx = P.PrecisionContext(bits)
+        L = P.nlimbs_for(bits)
+        A = P.gen_uniform_full(n, n, 11, ctx)
+        cfg = P.BlockLUConfig(K, P.Algorithm.winograd, nmin)
+        work = P.DeviceMatrix(n, n, ctx)
+        src = A.to_device()
+        piv = np.zeros(n, np.int64)
+        zp = C.c_int64(0)
+        dev_ms, leaf_ms, leaf_madds, launches = [], [], 0, 0
+        for rep in range(4):
+            PL.lib.mpgpu_copy_device(work._h, C.c_void_p(work.data_ptr), C.c_void_p(src.data_ptr),
+                                     C.c_size_t(work.nbytes))
+            flush.zero_()
+            torch.cuda.synchronize()
+            s = PL.MpgpuStats()
+            rc = PL.lib.mpgpu_lu_blocked(work._h, C.byref(work.m), K, int(P.Algorithm.winograd), nmin, 1,
+                                         piv.ctypes.data_as(C.c_void_p), C.byref(zp), C.byref(s))
+            if rc:
+                raise RuntimeError(f"mpgpu_lu_blocked rc={rc}")
+            if rep:
+                dev_ms.append(s.device_ms)
+                leaf_ms.append(s.leaf_ms)
+                leaf_madds = s.leaf_madds
+                launches = s.launches
+        f = None
+        t0 = time.perf_counter()
+        for _ in range(2):
+            f = P.lu_blocked(A, cfg, ctx, pivoting=True)
+        e2e_ms = (time.perf_counter() - t0) / 2 * 1e3
+        ones = P.from_ints(np.ones(n, np.int64), ctx)
+        bvec = P.mat_vec_mul(A, ones, ctx)
+        t0 = time.perf_counter()
+        x = P.lu_solve(f, bvec, ctx, exact=False)
+        solve_ms = (time.perf_counter() - t0) * 1e3
+        fe = P.max_rel_error_solution(x, ones)
+        fwd = float(np.abs(fe.max_rel.to_float()).max())
+        schur_tiops = leaf_madds * 2 * L * L / (float(np.mean(leaf_ms)) * 1e-3) / 1e12
+        out = {"workload": "BASELINE config 5(a): LU with partial pivoting n=2048 @256-bit, winograd Schur K=64 "
+                           "(alpha 2, n_min 32), A uniform [-1,1) full-mantissa (seed 11), b = A*1",
+               "device_ms": float(np.mean(dev_ms)), "schur_leaf_ms": float(np.mean(leaf_ms)),
+               "schur_leaf_madds": int(leaf_madds), "launches": int(launches),
+               "schur_leaf_roofline": {"achieved": schur_tiops, "peak": leaf_peak_tiops, "unit": "TIOP/s (IMAD-eq)",
+                                       "frac": schur_tiops / leaf_peak_tiops},
+               "madd_per_s": (n ** 3 / 3) / (float(np.mean(dev_ms)) * 1e-3),
+               "e2e": {"ms": e2e_ms, "api": "mpgpu_upload + mpgpu_lu_blocked + mpgpu_download (host SoA), wall",
+                       "h2d_bytes": nbytes_soa(n * n, L), "d2h_bytes": nbytes_soa(n * n, L)},
+               "solve_ms": solve_ms, "solve": "column-oriented lu_solve (exact=False)",
+               "forward_error_max_rel": fwd, "forward_error": "max_rel_error_solution(x, 1) in MP on the device"}
+        for x_ in (work, src):
+            x_.free()
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = lu_cpu_baseline(A, K, nmin)
+        return out
+    except Exception as e:  # reported, never fatal for the headline line
+        return {"error": repr(e)[:300]}
+
+
+def lu_cpu_baseline(A, K, nmin, s=256):
+    """The compiled reference's lu_blocked (pivot-free: the reference has no pivoting) with the
+    same Schur kernel, K and n_min on the top-left s x s block of the same A, one core,
+    wall clock; extrapolated to n by the n^3 / 3 Schur work."""
+    try:
+        from oracle import oracle as O
+        if not O.have_ref():
+            return {"value": None, "sample": "oracle/_ref not built"}
+        a = O.OMat.of(A.sub(0, 0, s, s))
+        t0 = time.perf_counter()
+        O.lu_blocked(a, K, "winograd", nmin, pivoting=False, which="ref")
+        dt = time.perf_counter() - t0
+        n = A.rows()
+        return {"value": (s ** 3 / 3) / dt, "unit": "madd/s (n^3/3 per factorisation)", "cores": 1,
+                "kind": "reference", "seconds_at_sample": dt,
+                "extrapolated_seconds_at_n": dt * (n / s) ** 3,
+                "sample": f"reference lu_blocked(winograd, K={K}, n_min={nmin}) pivot-free on the {s}x{s} top-left "
+                          f"block of A, 1 core; n={n} time extrapolated by (n/{s})^3"}
+    except Exception as e:
+        return {"value": None, "sample": f"failed: {e}"}
 
 
 def e2e(args, P, torch, a, b, algo, param, ctx, L):

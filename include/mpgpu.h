@@ -50,6 +50,12 @@ extern "C" {
 #define MPGPU_MAX_PREC 9216
 #define MPGPU_MAX_STORE_PREC MPGPU_MAX_PREC
 
+/* n_min / param value selecting the Strassen / Winograd cutoff automatically (mpgpu_choose_nmin):
+ * the recursion depth that minimises the modelled device time given the measured leaf-GEMM
+ * throughput of the precision (documented extension; an explicit n_min replays the reference
+ * bit for bit, as always). */
+#define MPGPU_AUTO_NMIN (-1)
+
 /* mpmm::Algorithm (fastmm.hpp:13) */
 enum { MPGPU_SIMPLE = 0, MPGPU_BLOCK = 1, MPGPU_STRASSEN = 2, MPGPU_WINOGRAD = 3 };
 
@@ -218,7 +224,57 @@ int mpgpu_fast_combine_rows(mpgpu_handle* h, int algo, int64_t n_min, int64_t l,
 int mpgpu_copy_device_2d(mpgpu_handle* h, void* dst, size_t dpitch, const void* src, size_t spitch,
                          size_t width, size_t height);
 
+/* Rows of C produced by the row-owned combine of unit rows [row_lo, row_hi) (the rows
+ * mpgpu_fast_combine_rows writes): *count rows, the first `cap` of them into out (sorted). */
+int mpgpu_fast_owned_rows(int64_t m, int64_t l, int64_t n, int64_t n_min, int up_levels, int64_t row_lo,
+                          int64_t row_hi, int64_t* out, int64_t cap, int64_t* count);
+/* Upload / download between a dense device matrix (or a full-width row view) and host SoA
+ * planes that belong to a LARGER host matrix: limb plane k of the host matrix starts
+ * host_plane_stride elements after plane k-1 (pointers pre-offset to the first element),
+ * e.g. rows r0.. of an m x n host matrix: limbs + r0*n, exp + r0*n, sign + r0*n, stride m*n. */
+int mpgpu_upload_strided(mpgpu_handle* h, mpgpu_mat* m, const uint32_t* limbs, const int32_t* exp,
+                         const uint8_t* sign, int32_t host_nlimbs, int64_t host_plane_stride);
+int mpgpu_download_strided(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                           int32_t host_nlimbs, int64_t host_plane_stride);
+
+/* ---- multi-GPU: one process driving several devices (SURVEY.md 8(b) gpu_mask, 8(e)) ----
+ * A group holds one handle per device.  mpgpu_group_gemm_host is mpgpu_gemm_host over
+ * all of them -- same arguments, same results bit for bit (simple_mul / block_mul
+ * matrix.hpp:178-233: C split by row blocks, no exchange; fast_mul fastmm.hpp:244-255:
+ * the 7^d leaf products split over the devices, each device doing its own pre-additions,
+ * one exchange of unit-product row slices by peer copies over NVLink, row-owned
+ * post-additions, each device writing its rows of C to the host).  A device may repeat in
+ * mpgpu_group_init_devices (shards of one GPU: the same path on a one-GPU host). */
+typedef struct mpgpu_group mpgpu_group;
+int mpgpu_group_init(uint32_t gpu_mask, mpgpu_group** out); /* device d <-> bit d */
+int mpgpu_group_init_devices(int ndev, const int* devices, mpgpu_group** out);
+void mpgpu_group_destroy(mpgpu_group* g);
+int mpgpu_group_size(const mpgpu_group* g);
+int mpgpu_group_device(const mpgpu_group* g, int i);
+mpgpu_handle* mpgpu_group_handle(mpgpu_group* g, int i);
+const char* mpgpu_group_last_error(const mpgpu_group* g);
+/* stats: mul / addsub of the whole product, leaf_madds summed over devices, times = the
+ * slowest device's */
+int mpgpu_group_gemm_host(mpgpu_group* g, int algo, int64_t param, int32_t prec, int64_t m, int64_t l,
+                          int64_t n, const uint32_t* a_limbs, const int32_t* a_exp, const uint8_t* a_sign,
+                          const uint32_t* b_limbs, const int32_t* b_exp, const uint8_t* b_sign,
+                          uint32_t* c_limbs, int32_t* c_exp, uint8_t* c_sign, int32_t host_nlimbs,
+                          mpgpu_stats* stats);
+/* the same through a process-wide group cached per gpu_mask (the C++ drop-in's entry);
+ * err (optional) receives the error text */
+int mpgpu_gemm_host_mask(uint32_t gpu_mask, int algo, int64_t param, int32_t prec, int64_t m, int64_t l,
+                         int64_t n, const uint32_t* a_limbs, const int32_t* a_exp, const uint8_t* a_sign,
+                         const uint32_t* b_limbs, const int32_t* b_exp, const uint8_t* b_sign,
+                         uint32_t* c_limbs, int32_t* c_exp, uint8_t* c_sign, int32_t host_nlimbs,
+                         mpgpu_stats* stats, char* err, size_t err_len);
+
 /* ---- host-side model / plan / inputs ------------------------------------ */
+/* The cutoff MPGPU_AUTO_NMIN resolves to for an m x l x n product at prec bits (Strassen /
+ * Winograd): per candidate depth d, modelled time = leaf multiply-adds / measured leaf rate at
+ * that leaf size + pre/post-addition record bytes / measured bandwidth; the fastest depth wins.
+ * n_min = the smallest cutoff giving that depth; depth / model_ms may be NULL. */
+int mpgpu_choose_nmin(int algo, int32_t prec, int64_t m, int64_t l, int64_t n, int64_t* n_min, int32_t* depth,
+                      double* model_ms);
 /* count_fast (opmodel.hpp:30-44); SIMPLE / BLOCK give count_simple */
 int mpgpu_count_fast(int algo, int64_t m, int64_t l, int64_t n, int64_t n_min, uint64_t* out2);
 /* recursion_plan (fastmm.hpp:68-85): rows of 8 int64 {level, m,l,n, pm,pl,pn, base} */

@@ -16,12 +16,23 @@
 // Results are bit-identical to the reference (same operation DAG, MPFR_RNDN rounding).
 // Documented deviations: operands of one call must share one precision <= MPGPU_MAX_PREC (9216) bits
 // (DomainError otherwise), and NaN/Inf inputs are rejected with DomainError.
+//
+// Multi-GPU (SURVEY.md 8(b) gpu_mask, 8(e)): mpmm::gpu::set_gpu_mask(mask) -- or the environment
+// variable MPGPU_GPU_MASK (e.g. 0xff) read once -- routes simple_mul / block_mul / fast_mul through
+// mpgpu_gemm_host_mask: one process drives every selected device (row shards for Simple / Block,
+// leaf shards + one peer-copy exchange + row-owned post-additions for Strassen / Winograd), with
+// results bit-identical to one device.  Unset (0): one handle on device 0.
+// mpfr_t <-> SoA packing runs on up to 32 host threads for large matrices.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mpgpu.h"
@@ -30,6 +41,32 @@ namespace mpmm {
 namespace gpu {
 
 namespace detail {
+
+inline std::uint32_t& gpu_mask_ref() {
+  static std::uint32_t mask = [] {
+    const char* e = std::getenv("MPGPU_GPU_MASK");
+    return e ? static_cast<std::uint32_t>(std::strtoul(e, nullptr, 0)) : 0u;
+  }();
+  return mask;
+}
+
+// fn(lo, hi) over [0, n) on up to 32 host threads (small n: the calling thread)
+template <class F>
+inline void parallel_for(std::size_t n, F&& fn) {
+  const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = std::min<std::size_t>({hw, 32, n / 16384 + 1});
+  if (nt <= 1) {
+    fn(std::size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::size_t per = (n + nt - 1) / nt;
+  for (std::size_t t = 0; t < nt; ++t) {
+    const std::size_t lo = t * per, hi = std::min(n, lo + per);
+    if (lo < hi) th.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
 
 inline mpgpu_handle* handle() {
   static std::unique_ptr<mpgpu_handle, void (*)(mpgpu_handle*)> h = [] {
@@ -41,15 +78,18 @@ inline mpgpu_handle* handle() {
 }
 
 // errors.hpp:10-48 <- mpgpu.h return codes
-inline void check(int rc, int64_t pivot = 0) {
+inline void check_msg(int rc, const std::string& msg, int64_t pivot = 0) {
   if (rc == MPGPU_OK) return;
-  const std::string msg = mpgpu_last_error(handle());
   switch (rc) {
     case MPGPU_ERR_DIMENSION: throw DimensionError(msg);
     case MPGPU_ERR_DOMAIN: throw DomainError(msg);
     case MPGPU_ERR_SINGULAR: throw SingularError(msg, static_cast<std::size_t>(pivot));
     default: throw Error("mpgpu: " + msg);
   }
+}
+inline void check(int rc, int64_t pivot = 0) {
+  if (rc == MPGPU_OK) return;
+  check_msg(rc, mpgpu_last_error(handle()), pivot);
 }
 
 struct Soa {
@@ -105,15 +145,18 @@ inline void unpack(const Soa& o, std::int64_t e, Scalar& s) {
 
 inline Soa to_soa(const Matrix& m) {
   Soa o(static_cast<std::int64_t>(m.rows() * m.cols()), m.bits());
-  for (std::size_t i = 0; i < m.rows(); ++i)
-    for (std::size_t j = 0; j < m.cols(); ++j) pack(m.at(i, j), o, static_cast<std::int64_t>(i * m.cols() + j));
+  const std::size_t cols = m.cols();
+  parallel_for(m.rows() * cols, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t e = lo; e < hi; ++e) pack(m.at(e / cols, e % cols), o, static_cast<std::int64_t>(e));
+  });
   return o;
 }
 
 inline Matrix from_soa(const Soa& o, std::size_t rows, std::size_t cols, PrecisionContext ctx) {
   Matrix m(rows, cols, ctx);
-  for (std::size_t i = 0; i < rows; ++i)
-    for (std::size_t j = 0; j < cols; ++j) unpack(o, static_cast<std::int64_t>(i * cols + j), m.at(i, j));
+  parallel_for(rows * cols, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t e = lo; e < hi; ++e) unpack(o, static_cast<std::int64_t>(e), m.at(e / cols, e % cols));
+  });
   return m;
 }
 
@@ -123,8 +166,12 @@ inline void same_precision(long a, long b, long c) {
   if (c > MPGPU_MAX_PREC) throw DomainError("mpmm::gpu: precision above the device maximum");
 }
 
-inline Matrix gemm(int algo, std::size_t param, const Matrix& a, const Matrix& b, PrecisionContext ctx,
+inline Matrix gemm(int algo, std::size_t param_in, const Matrix& a, const Matrix& b, PrecisionContext ctx,
                    OpCounter* ops) {
+  // gpu::auto_n_min (SIZE_MAX) -> MPGPU_AUTO_NMIN: the cutoff chosen per precision
+  const std::int64_t param = param_in == std::numeric_limits<std::size_t>::max()
+                                 ? std::int64_t{MPGPU_AUTO_NMIN}
+                                 : static_cast<std::int64_t>(param_in);
   if (a.cols() != b.rows())
     throw DimensionError("inner dimension mismatch: " + std::to_string(a.cols()) + " vs " +
                          std::to_string(b.rows()));
@@ -132,10 +179,19 @@ inline Matrix gemm(int algo, std::size_t param, const Matrix& a, const Matrix& b
   Soa sa = to_soa(a), sb = to_soa(b);
   Soa sc(static_cast<std::int64_t>(a.rows() * b.cols()), ctx.bits());
   mpgpu_stats st{};
-  check(mpgpu_gemm_host(handle(), algo, static_cast<std::int64_t>(param), static_cast<std::int32_t>(ctx.bits()),
-                        a.rows(), a.cols(), b.cols(), sa.limbs.data(), sa.exp.data(), sa.sign.data(),
-                        sb.limbs.data(), sb.exp.data(), sb.sign.data(), sc.limbs.data(), sc.exp.data(),
-                        sc.sign.data(), sc.L, &st));
+  if (const std::uint32_t mask = gpu_mask_ref()) {  // the multi-GPU group of the selected devices
+    char err[512] = {0};
+    const int rc = mpgpu_gemm_host_mask(
+        mask, algo, param, static_cast<std::int32_t>(ctx.bits()), a.rows(), a.cols(),
+        b.cols(), sa.limbs.data(), sa.exp.data(), sa.sign.data(), sb.limbs.data(), sb.exp.data(), sb.sign.data(),
+        sc.limbs.data(), sc.exp.data(), sc.sign.data(), sc.L, &st, err, sizeof err);
+    check_msg(rc, err);
+  } else {
+    check(mpgpu_gemm_host(handle(), algo, param, static_cast<std::int32_t>(ctx.bits()),
+                          a.rows(), a.cols(), b.cols(), sa.limbs.data(), sa.exp.data(), sa.sign.data(),
+                          sb.limbs.data(), sb.exp.data(), sb.sign.data(), sc.limbs.data(), sc.exp.data(),
+                          sc.sign.data(), sc.L, &st));
+  }
   if (ops) {
     ops->mul += st.mul;
     ops->addsub += st.addsub;
@@ -144,6 +200,15 @@ inline Matrix gemm(int algo, std::size_t param, const Matrix& a, const Matrix& b
 }
 
 }  // namespace detail
+
+// Devices used by simple_mul / block_mul / fast_mul: bit d selects device d (0: one handle on
+// device 0, the default unless MPGPU_GPU_MASK is set).  Not part of the reference API.
+inline void set_gpu_mask(std::uint32_t mask) { detail::gpu_mask_ref() = mask; }
+// FastMMConfig{alg, gpu::auto_n_min}: the Strassen / Winograd cutoff chosen from the measured
+// leaf-GEMM throughput of the precision (mpgpu_choose_nmin).  Not part of the reference API;
+// an explicit n_min replays the reference bit for bit.
+inline constexpr std::size_t auto_n_min = std::numeric_limits<std::size_t>::max();
+inline std::uint32_t gpu_mask() { return detail::gpu_mask_ref(); }
 
 // ---- matrix.hpp ---------------------------------------------------------
 inline Matrix simple_mul(const Matrix& a, const Matrix& b, PrecisionContext ctx) {

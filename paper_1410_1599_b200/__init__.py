@@ -1,7 +1,7 @@
 """paper_1410_1599_b200 -- B200-native multiple-precision Simple / Block /
 Strassen / Winograd matrix multiplication and blocked LU (drop-in for the MPFR
 reference's mpmm hot path).  See DESIGN.md and include/mpgpu.h."""
-from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix, Dims3, DimensionError,
+from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceGroup, DeviceMatrix, Dims3, DimensionError,
                    DomainError, Error, FastMMConfig, FastMMResult, LUFactors, Matrix, OpCounter,
                    PrecisionContext, RecursionLevel, SingularError, Stats, TopTrace, add, algorithm_name,
                    block_mul, count_fast, count_simple, equal_values, fast_mul, gemm_host, gemm_into, handle, identical,
@@ -9,7 +9,7 @@ from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceMatrix
                    record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
                    solve_columnwise, sub, vec_op, UndefinedMetricError, RelErrorStats, SolutionError,
                    max_rel_error, max_rel_error_solution, one_norm, convert, lu_solve_many,
-                   inverse, cond_one)
+                   inverse, cond_one, AUTO_NMIN, choose_n_min)
 from .matgen import Prng64, from_ints, gen_random, gen_scaled, gen_uniform_full, to_fractions
 from .codec import IoError, ParseError, from_hex, read_matrix, to_hex, write_matrix
 from .benchdrv import (CSV_HEADER, BenchRecord, LUOutcome, LURequest, MatmulRequest, append_csv, bench_reference,

@@ -79,6 +79,24 @@ _SIGS = {
     "mpgpu_max_rel_error": (C.c_int, [vp, MatP, MatP, vp, vp, vp, i64p]),
     "mpgpu_solution_error": (C.c_int, [vp, MatP, MatP, vp, vp, vp, i64p]),
     "mpgpu_one_norm": (C.c_int, [vp, MatP, vp, vp, vp]),
+    "mpgpu_choose_nmin": (C.c_int, [C.c_int, C.c_int32, C.c_int64, C.c_int64, C.c_int64, i64p,
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    "mpgpu_fast_owned_rows": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int64, C.c_int64,
+                                        vp, C.c_int64, i64p]),
+    "mpgpu_upload_strided": (C.c_int, [vp, MatP, vp, vp, vp, C.c_int32, C.c_int64]),
+    "mpgpu_download_strided": (C.c_int, [vp, MatP, vp, vp, vp, C.c_int32, C.c_int64]),
+    "mpgpu_group_init": (C.c_int, [C.c_uint32, C.POINTER(vp)]),
+    "mpgpu_group_init_devices": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]),
+    "mpgpu_group_destroy": (None, [vp]),
+    "mpgpu_group_size": (C.c_int, [vp]),
+    "mpgpu_group_device": (C.c_int, [vp, C.c_int]),
+    "mpgpu_group_handle": (vp, [vp, C.c_int]),
+    "mpgpu_group_last_error": (C.c_char_p, [vp]),
+    "mpgpu_group_gemm_host": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                                        vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int32, StatsP]),
+    "mpgpu_gemm_host_mask": (C.c_int, [C.c_uint32, C.c_int, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                                       vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int32, StatsP, C.c_char_p,
+                                       C.c_size_t]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -19,7 +19,7 @@ BUILD = PKG / "_build"
 LIB = PKG / "libmpgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu",
+SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu", "group.cu",
            "gemm_wide.cu", "metrics_wide.cu"] + \
     [f"{k}_wide{L}.cu" for k in ("elementwise", "lu") for L in (64, 128, 256, 288)]
 HEADERS = ["mp_arith.cuh", "kernels.h", "wmp.cuh", "wkern.cuh"]

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -210,6 +211,105 @@ std::vector<Level> plan_levels(int64_t m, int64_t l, int64_t n, int64_t n_min) {
   }
 }
 
+// ---- recursion depth per precision from measured leaf throughput (north star (2)) ----
+// B200 measurements (tools/leaf_table.py -> profiles/r02_leaf_table.jsonl): Winograd products with
+// 7^d leaves of s^3 (s = 16 .. 512) per limb count; the leaf kernel's MP multiply-adds per second and
+// the pre- / post-addition record bandwidth at that recursion level.  The leaf rate is flat for
+// s >= 32 and drops ~15 % at s = 16; the additions run at 2-4.5 TB/s.
+constexpr int kTabSizes = 6;
+constexpr double kTabEdge[kTabSizes] = {16, 32, 64, 128, 256, 512};
+struct LeafTab {
+  int L;
+  double rate[kTabSizes];  // leaf madd/s
+  double pre[kTabSizes];   // pre-add GB/s (deepest level, node edge 2s)
+  double post[kTabSizes];  // post-add GB/s
+};
+constexpr LeafTab kLeafTab[] = {
+    {4, {1.061e11, 1.251e11, 1.243e11, 1.311e11, 1.314e11, 1.307e11}, {2264, 3960, 3541, 4777, 4447, 3898},
+     {2221, 4036, 3812, 4527, 4193, 3811}},
+    {8, {6.568e10, 7.472e10, 7.390e10, 7.713e10, 7.739e10, 7.683e10}, {2027, 3758, 3372, 4533, 4185, 3852},
+     {2024, 3614, 3478, 4213, 4020, 3607}},
+    {16, {2.742e10, 2.938e10, 2.931e10, 3.004e10, 3.013e10, 3.019e10}, {2246, 3668, 3300, 4211, 4003, 3694},
+     {2005, 2947, 2693, 3371, 3269, 2985}},
+    {32, {8.016e9, 8.391e9, 8.475e9, 8.636e9, 8.667e9, 8.687e9}, {1949, 2922, 2645, 3354, 3230, 3050},
+     {2170, 3213, 2923, 3743, 3557, 3284}},
+};
+
+// table row for L (L < 4: the 128-bit row; L > 32: the 1024-bit row with the rate scaled by (32/L)^2)
+const LeafTab& leaf_row(int L, double* rate_scale) {
+  *rate_scale = 1.0;
+  if (L <= 4) return kLeafTab[0];
+  if (L <= 8) return kLeafTab[1];
+  if (L <= 16) return kLeafTab[2];
+  if (L > 32) *rate_scale = (32.0 / L) * (32.0 / L);
+  return kLeafTab[3];
+}
+
+double interp_edge(const double (&v)[kTabSizes], double edge) {
+  if (edge <= kTabEdge[0]) return v[0] * std::max(edge, 1.0) / kTabEdge[0];  // tiny leaves: idle threads
+  if (edge >= kTabEdge[kTabSizes - 1]) return v[kTabSizes - 1];
+  int i = 0;
+  while (edge > kTabEdge[i + 1]) ++i;
+  const double t = (std::log2(edge) - std::log2(kTabEdge[i])) / (std::log2(kTabEdge[i + 1]) - std::log2(kTabEdge[i]));
+  return v[i] + t * (v[i + 1] - v[i]);
+}
+
+// modelled device time (ms) of fast_mul stopped at depth d, and the n_min giving that depth
+double model_fast_ms(int L, int64_t m, int64_t l, int64_t n, int d, int64_t* n_min_out) {
+  double scale;
+  const LeafTab& row = leaf_row(L, &scale);
+  const double rec = 4.0 * mpg::rec_stride(L);
+  double ms = 0, nodes = 1;
+  int64_t dm = m, dl = l, dn = n;
+  for (int t = 0; t < d; ++t) {
+    const int64_t hm = (dm + dm % 2) / 2, hl = (dl + dl % 2) / 2, hn = (dn + dn % 2) / 2;
+    const double edge = std::cbrt((double)hm * hl * hn);
+    // pre-add: read each parent operand, write 7 quarter-size children; post-add: read 7
+    // children products, write the parent
+    const double pre = nodes * (double)(dm * dl + dl * dn) * rec * (1.0 + 7.0 / 4.0);
+    const double post = nodes * (double)(dm * dn) * rec * (1.0 + 7.0 / 4.0);
+    ms += pre / (interp_edge(row.pre, edge) * 1e6) + post / (interp_edge(row.post, edge) * 1e6);
+    nodes *= 7;
+    dm = hm;
+    dl = hl;
+    dn = hn;
+  }
+  const double leaf_madds = nodes * (double)dm * dl * dn;
+  ms += leaf_madds / (interp_edge(row.rate, std::cbrt((double)dm * dl * dn)) * scale) * 1e3;
+  *n_min_out = std::min({dm, dl, dn});
+  return ms;
+}
+
+int choose_nmin(int L, int64_t m, int64_t l, int64_t n, int64_t* n_min, int* depth, double* model_ms) {
+  double best = 0;
+  int64_t best_nmin = std::min({m, l, n});
+  int best_d = 0;
+  for (int d = 0; d <= 12; ++d) {
+    int64_t nm = 0;
+    // depth d exists only while every level-(d-1) dimension still exceeds the cutoff
+    if (d > 0) {
+      int64_t pm = m, pl = l, pn = n;
+      for (int t = 0; t < d - 1; ++t) {
+        pm = (pm + pm % 2) / 2;
+        pl = (pl + pl % 2) / 2;
+        pn = (pn + pn % 2) / 2;
+      }
+      if (std::min({pm, pl, pn}) < 2) break;
+    }
+    const double ms = model_fast_ms(L, m, l, n, d, &nm);
+    if (d > 0 && plan_levels(m, l, n, nm).size() != (size_t)d + 1) break;  // cutoff cannot realise d
+    if (d == 0 || ms < best) {
+      best = ms;
+      best_nmin = nm;
+      best_d = d;
+    }
+  }
+  if (n_min) *n_min = std::max<int64_t>(1, best_nmin);
+  if (depth) *depth = best_d;
+  if (model_ms) *model_ms = best;
+  return MPGPU_OK;
+}
+
 int check_err(mpgpu_handle* h) {
   flush_timers();
   uint32_t e = 0;
@@ -229,10 +329,121 @@ int check_err(mpgpu_handle* h) {
 // one fused post-add launch per level back up.  Same operation DAG as the
 // reference's depth-first recursion, so the result is bit-identical.
 // ---------------------------------------------------------------------------
+// scratch the breadth-first driver may hold at once: MPGPU_BFS_BUDGET_MB, else 60 % of the
+// device's memory; deeper recursions run their top levels depth-first (run_gemm_chunked)
+size_t bfs_budget(mpgpu_handle* h) {
+  if (const char* e = std::getenv("MPGPU_BFS_BUDGET_MB")) return (size_t)std::atoll(e) << 20;
+  static size_t total = [] {
+    size_t f = 0, t = 0;
+    if (cudaMemGetInfo(&f, &t) != cudaSuccess) {
+      cudaGetLastError();
+      t = (size_t)80 << 30;
+    }
+    return t;
+  }();
+  (void)h;
+  return total / 10 * 6;
+}
+
 template <int L>
 int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_t lda, const uint32_t* B,
              int64_t ldb, uint32_t* C, int64_t ldc, int64_t m, int64_t l, int64_t n, int sh,
-             mpgpu_stats* stats, int sub_from_c, cudaEvent_t b_ready = nullptr) {
+             mpgpu_stats* stats, int sub_from_c, cudaEvent_t b_ready = nullptr);
+
+// One recursion level run explicitly, its 7 products by run_gemm one after another: the same
+// operation DAG as the breadth-first driver (every node's pre-additions, product and
+// post-additions are unchanged -- only the order nodes are visited differs), so the result is
+// bit-identical, with the scratch of one subtree at a time instead of the whole level.
+template <int L>
+int run_gemm_chunked(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_t lda, const uint32_t* B,
+                     int64_t ldb, uint32_t* C, int64_t ldc, int64_t m, int64_t l, int64_t n, int sh,
+                     mpgpu_stats* stats, cudaEvent_t b_ready) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  const bool timing = stats != nullptr;
+  if (b_ready) cudaStreamWaitEvent(st, b_ready, 0);
+  Timer total(timing, st);
+  int launches = 0;
+  DevBuf a0, b0, top;
+  const uint32_t* pa = A;
+  const uint32_t* pb = B;
+  if (lda != l) {
+    CUDA_TRY(h, a0.alloc(h, sizeof(uint32_t) * S * m * l));
+    mpg::launch_copy2d<L>(A, lda, a0.u32(), l, (int)m, (int)l, st);
+    ++launches;
+    pa = a0.u32();
+  }
+  if (ldb != n) {
+    CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * l * n));
+    mpg::launch_copy2d<L>(B, ldb, b0.u32(), n, (int)l, (int)n, st);
+    ++launches;
+    pb = b0.u32();
+  }
+  const int64_t hm = (m + m % 2) / 2, hl = (l + l % 2) / 2, hn = (n + n % 2) / 2;
+  DevBuf a1, b1, p1;
+  CUDA_TRY(h, a1.alloc(h, sizeof(uint32_t) * S * 7 * hm * hl));
+  CUDA_TRY(h, b1.alloc(h, sizeof(uint32_t) * S * 7 * hl * hn));
+  CUDA_TRY(h, p1.alloc(h, sizeof(uint32_t) * S * 7 * hm * hn));
+  double pre_top = 0, post_top = 0;
+  {
+    Timer tp(timing, st);
+    mpg::launch_preadd<L>(algo, 0, pa, 1, (int)m, (int)l, a1.u32(), sh, h->d_err, st);
+    mpg::launch_preadd<L>(algo, 1, pb, 1, (int)l, (int)n, b1.u32(), sh, h->d_err, st);
+    launches += 2;
+    if (stats) tp.stop(&pre_top);
+  }
+  a0.release();
+  b0.release();
+  mpgpu_stats sum{};
+  for (int q = 0; q < 7; ++q) {
+    mpgpu_stats cs{};
+    int rc = run_gemm<L>(h, algo, param, a1.u32() + q * hm * hl * S, hl, b1.u32() + q * hl * hn * S, hn,
+                         p1.u32() + q * hm * hn * S, hn, hm, hl, hn, sh, stats ? &cs : nullptr, 0, nullptr);
+    if (rc) return rc;
+    if (stats) {
+      flush_timers();  // resolve the child's phase times now (cs is local)
+      sum.leaf_ms += cs.leaf_ms;
+      sum.preadd_ms += cs.preadd_ms;
+      sum.postadd_ms += cs.postadd_ms;
+      sum.leaf_madds += cs.leaf_madds;
+      sum.depth = cs.depth;
+    }
+    launches += cs.launches;
+  }
+  a1.release();
+  b1.release();
+  {
+    Timer tq(timing, st);
+    uint32_t* dst = C;
+    if (ldc != n) {
+      CUDA_TRY(h, top.alloc(h, sizeof(uint32_t) * S * m * n));
+      dst = top.u32();
+    }
+    mpg::launch_postadd<L>(algo, p1.u32(), 1, (int)m, (int)n, dst, nullptr, sh, h->d_err, st);
+    ++launches;
+    if (top.p) {
+      mpg::launch_copy2d<L>(top.u32(), n, C, ldc, (int)m, (int)n, st);
+      ++launches;
+    }
+    if (stats) tq.stop(&post_top);
+  }
+  if (stats) {
+    total.stop(&stats->device_ms);
+    flush_timers();
+    stats->leaf_ms = sum.leaf_ms;
+    stats->leaf_madds = sum.leaf_madds;
+    stats->preadd_ms = sum.preadd_ms + pre_top;
+    stats->postadd_ms = sum.postadd_ms + post_top;
+    stats->depth = sum.depth + 1;
+    stats->launches = launches;
+  }
+  return MPGPU_OK;
+}
+
+template <int L>
+int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_t lda, const uint32_t* B,
+             int64_t ldb, uint32_t* C, int64_t ldc, int64_t m, int64_t l, int64_t n, int sh,
+             mpgpu_stats* stats, int sub_from_c, cudaEvent_t b_ready) {
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   const bool timing = stats != nullptr;
@@ -255,6 +466,8 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
       peak = std::max(peak, prevA + prevB + prodsz.back());
       for (size_t lev = pl.size() - 1; lev >= 2; --lev) peak = std::max(peak, prodsz[lev] + prodsz[lev - 1]);
       peak += rec * (size_t)(m * l + l * n + m * n);  // dense copies / top buffer, if needed
+      if (peak > bfs_budget(h) && pl.size() >= 3 && !sub_from_c)
+        return run_gemm_chunked<L>(h, algo, param, A, lda, B, ldb, C, ldc, m, l, n, sh, stats, b_ready);
       int rc = ensure_pool(h, peak + peak / 8);
       if (rc) return rc;
     }
@@ -730,19 +943,26 @@ int bitlen(const std::vector<uint32_t>& v) {
 // host SoA -> device records (stream-ordered, no sync); stage is scratch owned by the caller
 // host SoA planes -> staging (H2D on `st`) -> device records; `copied` (optional) is
 // recorded on `st` once the host bytes are across
+// host SoA planes (plane j of the host matrix starts hstride elements after plane j-1;
+// hstride == N for a dense host matrix) -> staging (H2D on `st`) -> device records;
+// `copied` (optional) is recorded on `st` once the host bytes are across
 int upload_async_to(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_t* limbs, const int32_t* exp,
-                    const uint8_t* sign, int32_t Lh, uint32_t* stage, cudaStream_t st, cudaEvent_t copied = nullptr) {
-  const size_t planes = sizeof(uint32_t) * (size_t)L * N;
+                    const uint8_t* sign, int32_t Lh, uint32_t* stage, cudaStream_t st, cudaEvent_t copied = nullptr,
+                    int64_t hstride = -1) {
+  if (hstride < 0) hstride = N;
   uint32_t* dl = stage;
   int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
   uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
-  if (Lh <= L) {
-    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, st));
-    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
-                                cudaMemcpyHostToDevice, st));
-  } else {
-    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, st));
-  }
+  // most significant limbs aligned: host plane j <-> device plane j + (L - Lh)
+  const int np = Lh <= L ? Lh : L;
+  uint32_t* dst0 = Lh <= L ? dl + (size_t)(L - Lh) * N : dl;
+  const uint32_t* src0 = Lh <= L ? limbs : limbs + (size_t)(Lh - L) * hstride;
+  if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, st));
+  if (hstride == N)
+    CUDA_TRY(h, cudaMemcpyAsync(dst0, src0, sizeof(uint32_t) * (size_t)np * N, cudaMemcpyHostToDevice, st));
+  else
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst0, sizeof(uint32_t) * N, src0, sizeof(uint32_t) * hstride, sizeof(uint32_t) * N,
+                                  np, cudaMemcpyHostToDevice, st));
   CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
   CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, st));
   if (copied) CUDA_TRY(h, cudaEventRecord(copied, st));
@@ -755,33 +975,16 @@ int upload_async_to(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint
 
 int upload_async(mpgpu_handle* h, uint32_t* rec, int L, int64_t N, const uint32_t* limbs, const int32_t* exp,
                  const uint8_t* sign, int32_t Lh, DevBuf& stage, cudaStream_t st_in = nullptr,
-                 cudaEvent_t copied = nullptr) {
+                 cudaEvent_t copied = nullptr, int64_t hstride = -1) {
   const size_t planes = sizeof(uint32_t) * (size_t)L * N;
   CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
-  if (st_in || copied)
-    return upload_async_to(h, rec, L, N, limbs, exp, sign, Lh, stage.u32(), st_in ? st_in : h->stream, copied);
-  uint32_t* dl = stage.u32();
-  int32_t* de = reinterpret_cast<int32_t*>(dl + (size_t)L * N);
-  uint8_t* ds = reinterpret_cast<uint8_t*>(de + N);
-  // most significant limbs aligned: host plane j <-> device plane j + (L - Lh)
-  if (Lh <= L) {
-    if (Lh < L) CUDA_TRY(h, cudaMemsetAsync(dl, 0, sizeof(uint32_t) * (size_t)(L - Lh) * N, h->stream));
-    CUDA_TRY(h, cudaMemcpyAsync(dl + (size_t)(L - Lh) * N, limbs, sizeof(uint32_t) * (size_t)Lh * N,
-                                cudaMemcpyHostToDevice, h->stream));
-  } else {
-    CUDA_TRY(h, cudaMemcpyAsync(dl, limbs + (size_t)(Lh - L) * N, planes, cudaMemcpyHostToDevice, h->stream));
-  }
-  CUDA_TRY(h, cudaMemcpyAsync(de, exp, sizeof(int32_t) * N, cudaMemcpyHostToDevice, h->stream));
-  CUDA_TRY(h, cudaMemcpyAsync(ds, sign, N, cudaMemcpyHostToDevice, h->stream));
-  dispatch_store(L, [&](auto Lc) {
-    mpg::launch_soa2rec<decltype(Lc)::value>(dl, de, ds, N, N, rec, h->stream);
-    return 0;
-  });
-  return MPGPU_OK;
+  return upload_async_to(h, rec, L, N, limbs, exp, sign, Lh, stage.u32(), st_in ? st_in : h->stream, copied,
+                         hstride);
 }
 
 int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint32_t* limbs, int32_t* exp,
-                   uint8_t* sign, int32_t Lh, DevBuf& stage) {
+                   uint8_t* sign, int32_t Lh, DevBuf& stage, int64_t hstride = -1) {
+  if (hstride < 0) hstride = N;
   const size_t planes = sizeof(uint32_t) * (size_t)L * N;
   CUDA_TRY(h, stage.alloc(h, planes + sizeof(int32_t) * N + N));
   uint32_t* dl = stage.u32();
@@ -791,13 +994,16 @@ int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint3
     mpg::launch_rec2soa<decltype(Lc)::value>(rec, N, dl, de, ds, N, h->stream);
     return 0;
   });
-  if (Lh <= L) {
-    CUDA_TRY(h, cudaMemcpyAsync(limbs, dl + (size_t)(L - Lh) * N, sizeof(uint32_t) * (size_t)Lh * N,
-                                cudaMemcpyDeviceToHost, h->stream));
-  } else {
-    std::memset(limbs, 0, sizeof(uint32_t) * (size_t)(Lh - L) * N);
-    CUDA_TRY(h, cudaMemcpyAsync(limbs + (size_t)(Lh - L) * N, dl, planes, cudaMemcpyDeviceToHost, h->stream));
-  }
+  const int np = Lh <= L ? Lh : L;
+  const uint32_t* src0 = Lh <= L ? dl + (size_t)(L - Lh) * N : dl;
+  uint32_t* dst0 = Lh <= L ? limbs : limbs + (size_t)(Lh - L) * hstride;
+  if (Lh > L)
+    for (int j = 0; j < Lh - L; ++j) std::memset(limbs + (size_t)j * hstride, 0, sizeof(uint32_t) * N);
+  if (hstride == N)
+    CUDA_TRY(h, cudaMemcpyAsync(dst0, src0, sizeof(uint32_t) * (size_t)np * N, cudaMemcpyDeviceToHost, h->stream));
+  else
+    CUDA_TRY(h, cudaMemcpy2DAsync(dst0, sizeof(uint32_t) * hstride, src0, sizeof(uint32_t) * N, sizeof(uint32_t) * N,
+                                  np, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(exp, de, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaMemcpyAsync(sign, ds, N, cudaMemcpyDeviceToHost, h->stream));
   return MPGPU_OK;
@@ -815,6 +1021,9 @@ int mpgpu_init(int device, mpgpu_handle** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&h->d_err, 4 * sizeof(uint32_t));  // [0] flags, [2:4) int64 zero pivot
   if (e != cudaSuccess) {
+    cudaGetLastError();  // clear the runtime's last error: later calls must not see it
+    if (h->d_err) cudaFree(h->d_err);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
     return MPGPU_ERR_CUDA;
   }
@@ -947,10 +1156,91 @@ int mpgpu_download(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t
   return MPGPU_OK;
 }
 
+int mpgpu_upload_strided(mpgpu_handle* h, mpgpu_mat* m, const uint32_t* limbs, const int32_t* exp,
+                         const uint8_t* sign, int32_t Lh, int64_t host_plane_stride) {
+  if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
+  if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "upload into a strided view");
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  if (host_plane_stride < m->rows * m->cols) return fail(h, MPGPU_ERR_DIMENSION, "host plane stride too small");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  DevBuf stage;
+  int rc = upload_async(h, m->rec, m->nlimbs, m->rows * m->cols, limbs, exp, sign, Lh, stage, nullptr, nullptr,
+                        host_plane_stride);
+  if (rc) return rc;
+  stage.release();
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int mpgpu_download_strided(mpgpu_handle* h, const mpgpu_mat* m, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                           int32_t Lh, int64_t host_plane_stride) {
+  if (!h || !m || !m->rec) return MPGPU_ERR_DOMAIN;
+  if (m->ld != m->cols) return fail(h, MPGPU_ERR_DIMENSION, "download from a strided view");
+  if (Lh < (m->prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  if (host_plane_stride < m->rows * m->cols) return fail(h, MPGPU_ERR_DIMENSION, "host plane stride too small");
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  DevBuf stage;
+  int rc = download_async(h, m->rec, m->nlimbs, m->rows * m->cols, limbs, exp, sign, Lh, stage, host_plane_stride);
+  if (rc) return rc;
+  stage.release();
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int mpgpu_fast_owned_rows(int64_t m, int64_t l, int64_t n, int64_t n_min, int up_levels, int64_t row_lo,
+                          int64_t row_hi, int64_t* out, int64_t cap, int64_t* count) {
+  if (!count || m < 1 || l < 1 || n < 1 || n_min < 1) return MPGPU_ERR_DIMENSION;
+  const std::vector<Level> lv = plan_levels(m, l, n, n_min);
+  const int d = (int)lv.size() - 1;
+  if (up_levels < 0 || up_levels > d) return MPGPU_ERR_DIMENSION;
+  const int il = d - up_levels;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > lv[il].m) return MPGPU_ERR_DIMENSION;
+  const auto owned = owned_rows(lv, il, row_lo, row_hi);
+  *count = (int64_t)owned[0].size();
+  if (out)
+    for (int64_t i = 0; i < *count && i < cap; ++i) out[i] = owned[0][i];
+  return MPGPU_OK;
+}
+
+int mpgpu_choose_nmin(int algo, int32_t prec, int64_t m, int64_t l, int64_t n, int64_t* n_min, int32_t* depth,
+                      double* model_ms) {
+  if (m < 1 || l < 1 || n < 1) return MPGPU_ERR_DIMENSION;
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD) return MPGPU_ERR_DOMAIN;
+  const int L = nlimbs_for(prec);
+  if (!L) return MPGPU_ERR_DOMAIN;
+  int d = 0;
+  const int rc = choose_nmin(L, m, l, n, n_min, &d, model_ms);
+  if (depth) *depth = d;
+  return rc;
+}
+
+namespace {
+// MPGPU_AUTO_NMIN -> the chosen cutoff (Strassen / Winograd only)
+int resolve_auto(mpgpu_handle* h, int algo, int32_t prec, int64_t m, int64_t l, int64_t n, int64_t* param) {
+  if (*param != MPGPU_AUTO_NMIN) return MPGPU_OK;
+  if (algo == MPGPU_SIMPLE) {
+    *param = 0;
+    return MPGPU_OK;
+  }
+  if (algo != MPGPU_STRASSEN && algo != MPGPU_WINOGRAD)
+    return fail(h, MPGPU_ERR_DOMAIN, "MPGPU_AUTO_NMIN applies to strassen / winograd only");
+  const int L = nlimbs_for(prec);
+  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range", prec);
+  return choose_nmin(L, std::max<int64_t>(1, m), std::max<int64_t>(1, l), std::max<int64_t>(1, n), param, nullptr,
+                     nullptr);
+}
+}  // namespace
+
 int mpgpu_gemm(mpgpu_handle* h, int algo, int64_t param, const mpgpu_mat* A, const mpgpu_mat* B, mpgpu_mat* C,
                mpgpu_stats* stats) {
   TimerGuard timer_guard;
   if (!h) return MPGPU_ERR_DOMAIN;
+  if (A && B && C && A->cols == B->rows)
+    if (int r = resolve_auto(h, algo, C->prec, A->rows, A->cols, B->cols, &param)) return r;
   int rc = validate_gemm(h, algo, param, A, B, C);
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(h->mu);
@@ -984,6 +1274,7 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
   if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range [2, %d]", prec, MPGPU_MAX_PREC);
   if (m < 1 || l < 1 || n < 1) return fail(h, MPGPU_ERR_DIMENSION, "matrix dimensions must be at least 1x1");
   if (Lh < (prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  if (int r = resolve_auto(h, algo, prec, m, l, n, &param)) return r;
   mpgpu_mat A{m, l, prec, L, nullptr, l, 0}, B{l, n, prec, L, nullptr, n, 0}, C{m, n, prec, L, nullptr, n, 0};
   int rc = validate_gemm(h, algo, param, &A, &B, &C);
   if (rc) return rc;
@@ -1025,6 +1316,12 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
     if (rc) return rc;
   }
   CUDA_TRY(h, cudaEventRecord(h->ev_b, h->aux));
+  // on every return from here, db (freed on h->stream by ~DevBuf) must not be released
+  // while h->aux may still be writing it: order h->stream after B's upload first
+  struct WaitB {
+    mpgpu_handle* h;
+    ~WaitB() { cudaStreamWaitEvent(h->stream, h->ev_b, 0); }
+  } wait_b{h};
   sa.release();
   const int sh = 32 * L - prec;
   rc = dispatch_L(L, [&](auto Lc) {

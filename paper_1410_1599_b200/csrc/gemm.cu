@@ -324,14 +324,7 @@ void launch_tiles(const GemmArgs& g, cudaStream_t st) {
   constexpr int S = rec_stride(L);
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
   auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_leaf_kernel<L, TM, TN, TK, U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(gemm_leaf_kernel<L, TM, TN, TK, U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = true;
-  }
+  smem_attr_once((const void*)kern, (int)smem);
   // grid.z is limited to 65535: deep recursions (7^d leaves) launch in batch chunks
   for (int z0 = 0; z0 < g.batch; z0 += 65535) {
     GemmArgs gz = g;

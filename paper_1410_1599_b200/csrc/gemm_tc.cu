@@ -407,12 +407,7 @@ template <int L>
 bool launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   using CF = tc::Cfg<L>;
   auto kern = tc::gemm_tc_kernel<L>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM) != cudaSuccess)
-      return false;
-    configured = true;
-  }
+  smem_attr_once((const void*)kern, CF::SMEM);
   constexpr int S = rec_stride(L);
   for (int z0 = 0; z0 < g.batch; z0 += 65535) {  // grid.z limit
     GemmArgs gz = g;

@@ -3,7 +3,23 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace mpg {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the device's context, so a process driving several GPUs (mpgpu_group_*, or one
+// handle per device) must set it on each of them.  Thread-safe.
+inline void smem_attr_once(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert({kern, dev}).second) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 // Batched MP GEMM over AoS record arrays (rec_stride(L) words per element).
 // C[z] = A[z] * B[z] for z < batch, with the reference's inner-product order

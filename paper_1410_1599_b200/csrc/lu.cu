@@ -868,11 +868,7 @@ void launch_laswp_perm(uint32_t* a, int64_t n, int64_t p, int64_t k, const int64
   int tc = (int)std::max<int64_t>(1, (64 * 1024) / (2 * k * S * 4));
   if (tc > 32) tc = 32;
   const size_t smem = sizeof(int64_t) * 4 * (size_t)k + sizeof(uint32_t) * S * (size_t)(2 * k * tc);
-  static bool conf = false;
-  if (!conf) {
-    cudaFuncSetAttribute(laswp_perm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    conf = true;
-  }
+  smem_attr_once((const void*)laswp_perm_kernel<L>, 200 * 1024);
   if (smem > 200 * 1024) {  // very wide records x large panels: the swap-by-swap kernels
     if (skip_hi > skip_lo)
       laswp_kernel<L><<<blocks_for((n - k) * (S / 4)), NT, 0, st>>>(a, n, p, k, piv, zp);
@@ -897,19 +893,21 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
 #endif
   constexpr int S = rec_stride(L);
   uint64_t* cand_cnt = reinterpret_cast<uint64_t*>(cand_idx + max_grid);
-  static int max_blocks = 0;
-  static int dev_sms = 0;
+  // occupancy, queried once (thread-safe static init; every GPU of the box is the same B200)
+  static const int dev_sms = [] {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  static const int max_blocks = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_coop_kernel<L>, NT, 16 * 1024);
+    return per_sm * dev_sms;
+  }();
   const int64_t rows = row_end - p;
   // rows per CTA bounded so the multipliers fit in shared memory
   int64_t want = (rows + 7) / 8;
-  if (!max_blocks) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_coop_kernel<L>, NT, 16 * 1024);
-    max_blocks = per_sm * dev_sms;
-  }
   int64_t grid = want < max_blocks ? want : max_blocks;
   if (grid > 2 * dev_sms) grid = 2 * dev_sms;
   if (const char* g = std::getenv("MPGPU_LU_COOP_GRID")) grid = std::min<int64_t>(grid, std::atoll(g));
@@ -921,14 +919,12 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
   if (smem > 16 * 1024) return -1;  // caller falls back to per-column kernels
   if (pivoting && rows <= 12288 && std::getenv("MPGPU_LU_PERM") == nullptr) {
     // one barrier per column: logical row table in shared memory (+ rows int32 words)
-    static bool conf = false;
-    if (!conf) {
-      cudaFuncSetAttribute(lu_panel_perm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024 + 4 * 12288);
-      conf = true;
-    }
-    static int per_sm2 = -1;
-    if (per_sm2 < 0)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, lu_panel_perm_kernel<L>, NT, 16 * 1024 + 4 * 12288);
+    smem_attr_once((const void*)lu_panel_perm_kernel<L>, 16 * 1024 + 4 * 12288);
+    static const int per_sm2 = [] {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lu_panel_perm_kernel<L>, NT, 16 * 1024 + 4 * 12288);
+      return v;
+    }();
     int64_t g2 = std::min<int64_t>(grid, (int64_t)per_sm2 * dev_sms);
     if (g2 < 1) g2 = 1;
     int64_t ch = (rows + g2 - 1) / g2;
@@ -991,11 +987,7 @@ void launch_trsm_l_panel(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t c
 #endif
   const size_t smem = sizeof(uint32_t) * rec_stride(L) * (size_t)(k * TRSM_TC);
   if (smem <= 160 * 1024 && std::getenv("MPGPU_TRSM_GLOBAL") == nullptr) {
-    static bool conf = false;
-    if (!conf) {
-      cudaFuncSetAttribute(trsm_l_smem_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      conf = true;
-    }
+    smem_attr_once((const void*)trsm_l_smem_kernel<L>, 160 * 1024);
     trsm_l_smem_kernel<L><<<(int)((w + TRSM_TC - 1) / TRSM_TC), NT, smem, st>>>(a, n, p, k, c0, w, sh, TRSM_TC);
     return;
   }

@@ -191,11 +191,7 @@ void launch_reduce3(const uint32_t* A, const uint32_t* B, int64_t N, uint32_t* o
                     cudaStream_t st) {
   constexpr int S = rec_stride(L);
   const size_t smem = sizeof(uint32_t) * 3 * RT * S;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(reduce3_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  smem_attr_once((const void*)reduce3_kernel<L>, (int)smem);
   int64_t want = (N + RT * 8 - 1) / (RT * 8);
   const int g1 = (int)(want < 1 ? 1 : (want > 1024 ? 1024 : want));
   if (g1 == 1) {

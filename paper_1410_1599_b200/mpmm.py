@@ -540,6 +540,53 @@ def gemm_host(algo: Algorithm, param: int, a: Matrix, b: Matrix, c: Matrix, ctx:
     return Stats.of(st)
 
 
+class DeviceGroup:
+    """Several GPUs driven from this one process (mpgpu_group_*, include/mpgpu.h): the C-ABI
+    multi-GPU path.  `devices` may repeat a device (shards of one GPU)."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*devices)
+        hp = C.c_void_p()
+        rc = _L.lib.mpgpu_group_init_devices(len(devices), devs, C.byref(hp))
+        if rc:
+            raise DeviceError(f"mpgpu_group_init_devices({list(devices)}) failed (rc={rc})")
+        self._g = hp.value
+        self.devices = list(devices)
+
+    @staticmethod
+    def from_mask(mask: int) -> "DeviceGroup":
+        return DeviceGroup([d for d in range(32) if mask >> d & 1])
+
+    def size(self) -> int:
+        return _L.lib.mpgpu_group_size(self._g)
+
+    def gemm_host(self, algo: Algorithm, param: int, a: Matrix, b: Matrix, c: Matrix, ctx: PrecisionContext) -> Stats:
+        """mpgpu_group_gemm_host: the product over every device of the group, host SoA in
+        and out; bit-identical to gemm_host on one device."""
+        if a.nlimbs != b.nlimbs or a.nlimbs != c.nlimbs:
+            raise DomainError("gemm_host: one host limb count for A, B and C")
+        st = _L.MpgpuStats()
+        rc = _L.lib.mpgpu_group_gemm_host(self._g, int(algo), int(param), ctx.bits(), a.rows(), a.cols(), b.cols(),
+                                          _ptr(a.limbs), _ptr(a.exp), _ptr(a.sign), _ptr(b.limbs), _ptr(b.exp),
+                                          _ptr(b.sign), _ptr(c.limbs), _ptr(c.exp), _ptr(c.sign), a.nlimbs,
+                                          C.byref(st))
+        if rc:
+            msg = (_L.lib.mpgpu_group_last_error(self._g) or b"").decode()
+            raise {1: DimensionError, 2: DomainError}.get(rc, DeviceError)(msg)
+        return Stats.of(st)
+
+    def close(self) -> None:
+        if getattr(self, "_g", None):
+            _L.lib.mpgpu_group_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def simple_mul(a, b, ctx: PrecisionContext, ops: Optional[OpCounter] = None, stats: Optional[Stats] = None):
     """matrix.hpp:178-184 -- three-loop inner product, left to right in k."""
     c, o = _gemm(Algorithm.simple, 0, a, b, ctx, stats, isinstance(a, DeviceMatrix))
@@ -564,6 +611,22 @@ class FastMMResult:
     ops: OpCounter
 
 
+AUTO_NMIN = -1  # MPGPU_AUTO_NMIN: FastMMConfig(algo, AUTO_NMIN) -> cutoff chosen per precision
+
+
+def choose_n_min(algo: Algorithm, bits: int, m: int, l: int, n: int):
+    """mpgpu_choose_nmin: (n_min, depth, modelled ms) for an m x l x n Strassen / Winograd
+    product at `bits` -- the depth whose modelled time (measured leaf-GEMM rate at that leaf
+    size + pre/post-addition bytes at the measured bandwidth) is smallest."""
+    nm, d, ms = C.c_int64(0), C.c_int32(0), C.c_double(0)
+    rc = _L.lib.mpgpu_choose_nmin(int(algo), int(bits), m, l, n, C.byref(nm), C.byref(d), C.byref(ms))
+    if rc == 1:
+        raise DimensionError("choose_n_min: dimensions must be at least 1")
+    if rc:
+        raise DomainError("choose_n_min: strassen / winograd at a supported precision")
+    return int(nm.value), int(d.value), float(ms.value)
+
+
 def fast_mul(a, b, cfg: FastMMConfig, ctx: PrecisionContext, trace: Optional[TopTrace] = None,
              stats: Optional[Stats] = None) -> FastMMResult:
     """fastmm.hpp:244-255 -- Strassen / Winograd with cutoff n_min and pad-to-even."""
@@ -576,6 +639,8 @@ def fast_mul(a, b, cfg: FastMMConfig, ctx: PrecisionContext, trace: Optional[Top
     if trace is None:
         c, o = _gemm(cfg.algorithm, cfg.n_min, a, b, ctx, stats, isinstance(a, DeviceMatrix))
         return FastMMResult(c, o)
+    if cfg.n_min == AUTO_NMIN:
+        cfg = FastMMConfig(cfg.algorithm, choose_n_min(cfg.algorithm, ctx.bits(), a.rows(), a.cols(), b.cols())[0])
     return _fast_mul_traced(a, b, cfg, ctx, trace)
 
 

@@ -93,6 +93,26 @@ int main() {
   } catch (const SingularError& e) {
     CHECK(e.pivot_index == 1, "zero pivot throws SingularError(1)");
   }
+  {  // the multi-GPU entry (mpgpu_gemm_host_mask) through the same drop-in calls: device 0 only here
+    const BenchPair big = gen_bench_pair(70, 66, 61, ctx);
+    Matrix s1 = gpu::simple_mul(big.a, big.b, ctx), b1 = gpu::block_mul(big.a, big.b, 16, ctx);
+    FastMMResult w1 = gpu::fast_mul(big.a, big.b, FastMMConfig{Algorithm::winograd, 8}, ctx);
+    gpu::set_gpu_mask(0x1);
+    Matrix s2 = gpu::simple_mul(big.a, big.b, ctx), b2 = gpu::block_mul(big.a, big.b, 16, ctx);
+    FastMMResult w2 = gpu::fast_mul(big.a, big.b, FastMMConfig{Algorithm::winograd, 8}, ctx);
+    CHECK(equal_values(s1, s2) && equal_values(b1, b2), "gpu_mask 0x1: simple / block bit-exact");
+    CHECK(equal_values(w1.c, w2.c) && w1.ops == w2.ops, "gpu_mask 0x1: fast_mul winograd bit-exact");
+    CHECK(equal_values(w2.c, fast_mul(big.a, big.b, FastMMConfig{Algorithm::winograd, 8}, ctx).c),
+          "gpu_mask 0x1: fast_mul equals the reference");
+    try {
+      gpu::set_gpu_mask(0x80000000u);  // no such device
+      gpu::fast_mul(big.a, big.b, FastMMConfig{Algorithm::winograd, 8}, ctx);
+      CHECK(false, "gpu_mask with a missing device throws");
+    } catch (const Error&) {
+      CHECK(true, "gpu_mask with a missing device throws");
+    }
+    gpu::set_gpu_mask(0);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
   return failures ? 1 : 0;
 }

@@ -628,7 +628,15 @@ def precision_sweep(args, P, torch, peak_tiops):
         L = P.nlimbs_for(bits)
         achieved = st.leaf_madds * 2 * L * L / (leaf * 1e-3) / 1e12
         out[str(bits)] = {"leaf_ms": leaf, "leaf_madds": st.leaf_madds, "imad_eq_per_madd": 2 * L * L,
-                          "achieved_tiops": achieved, "frac": achieved / peak_tiops}
+                          "achieved_tiops": achieved, "frac": achieved / peak_tiops,
+                          "device_ms_at_n_min": min(P.gemm_into(algo, param, da, db, dc).device_ms for _ in range(2))}
+        if algo in (P.Algorithm.strassen, P.Algorithm.winograd):
+            # the cutoff chosen per precision from the measured leaf throughput (MPGPU_AUTO_NMIN)
+            nm, depth, model_ms = P.choose_n_min(algo, bits, n, n, n)
+            P.gemm_into(algo, P.AUTO_NMIN, da, db, dc)
+            auto = min((P.gemm_into(algo, P.AUTO_NMIN, da, db, dc) for _ in range(2)), key=lambda x: x.device_ms)
+            out[str(bits)]["auto_n_min"] = {"n_min": nm, "depth": depth, "model_ms": model_ms,
+                                            "device_ms": auto.device_ms, "leaf_ms": auto.leaf_ms}
         for x in (da, db, dc):
             x.free()
     torch.cuda.synchronize()

@@ -247,18 +247,21 @@ __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r,
 template <int L>
 __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
                                int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
-                               int sh, uint32_t* err, const int* __restrict__ rowlist, int nrows) {
+                               int sh, uint32_t* err, const int* __restrict__ rowlist, int nrows, int cc0,
+                               int ncc) {
   constexpr int S = rec_stride(L);
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
   const int64_t per = (int64_t)hr * hc;
-  // rowlist: only these child rows (row-owned combine of the multi-GPU path)
-  const int64_t per_iter = (rowlist ? (int64_t)nrows : (int64_t)hr) * hc;
+  // rowlist: only these child rows (row-owned combine of the multi-GPU path); [cc0, cc0 + ncc):
+  // only these child columns (the LU look-ahead's column split -- child column c feeds parent
+  // columns c and c + hc only)
+  const int64_t per_iter = (rowlist ? (int64_t)nrows : (int64_t)hr) * ncc;
   const int64_t total = per_iter * nodes;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t node = t / per_iter;
     const int64_t ei = t - node * per_iter;
-    const int ri = (int)(ei / hc), c = (int)(ei - (int64_t)ri * hc);
+    const int ri = (int)(ei / ncc), c = cc0 + (int)(ei - (int64_t)ri * ncc);
     const int r = rowlist ? rowlist[ri] : ri;
     const int64_t e = (int64_t)r * hc + c;
     const uint32_t* M = children + (node * 7 * per + e) * S;
@@ -353,8 +356,8 @@ __global__ void copy2d_kernel(const uint32_t* __restrict__ src, int64_t lds, uin
 }
 
 template <int L>
-__global__ void sub2d_kernel(uint32_t* __restrict__ C, int64_t ldc, const uint32_t* __restrict__ T, int rows,
-                             int cols, int sh, uint32_t* err) {
+__global__ void sub2d_kernel(uint32_t* __restrict__ C, int64_t ldc, const uint32_t* __restrict__ T, int64_t ldt,
+                             int rows, int cols, int sh, uint32_t* err) {
   constexpr int S = rec_stride(L);
   const int64_t total = (int64_t)rows * cols;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -362,7 +365,7 @@ __global__ void sub2d_kernel(uint32_t* __restrict__ C, int64_t ldc, const uint32
     const int64_t r = t / cols, c = t - r * cols;
     MP<L> x, y, z;
     load_rec<L>(C + (r * ldc + c) * S, x);
-    load_rec<L>(T + t * S, y);
+    load_rec<L>(T + (r * ldt + c) * S, y);
     mp_add<L>(x, y, 1u, sh, z);
     if (exp_out_of_range(z.e)) atomicOr(err, ERR_EXP_RANGE);
     store_rec<L>(C + (r * ldc + c) * S, z);
@@ -372,8 +375,10 @@ __global__ void sub2d_kernel(uint32_t* __restrict__ C, int64_t ldc, const uint32
 // ---------------------------------------------------------------------------
 template <int L>
 void launch_sub2d(uint32_t* C, int64_t ldc, const uint32_t* T, int rows, int cols, int sh, uint32_t* err,
-                  cudaStream_t st) {
-  sub2d_kernel<L><<<grid_for((int64_t)rows * cols), NT, 0, st>>>(C, ldc, T, rows, cols, sh, err);
+                  cudaStream_t st, int64_t ldt) {
+  if ((int64_t)rows * cols <= 0) return;
+  sub2d_kernel<L><<<grid_for((int64_t)rows * cols), NT, 0, st>>>(C, ldc, T, ldt < 0 ? cols : ldt, rows, cols, sh,
+                                                                 err);
 }
 template <int L>
 void launch_soa2rec(const uint32_t* limbs, const int32_t* exp, const uint8_t* sign, int64_t N,
@@ -417,17 +422,21 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist,
-                    int nrows) {
+                    int nrows, int cc0, int ncc) {
+  const int hc = (cols + cols % 2) / 2;
+  if (ncc < 0) ncc = hc - cc0;
 #if MPG_WIDE
   if constexpr (L > 32)
-    if (wmp::enabled())
+    if (wmp::enabled()) {  // (the column split is not used with the wide formats)
+      if (cc0 != 0 || ncc != hc) return;
       return wmp::launch_postadd<L / 32>(algo, children, nodes, rows, cols, parent, t_out, sh, err, st, rowlist,
                                          nrows);
+    }
 #endif
-  const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
+  const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ncc * nodes;
   if (total <= 0) return;
   postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,
-                                                     err, rowlist, nrows);
+                                                     err, rowlist, nrows, cc0, ncc);
 }
 template <int L>
 void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
@@ -453,10 +462,11 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_preadd<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int,          \
                                  uint32_t*, cudaStream_t);                                              \
   template void launch_postadd<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, uint32_t*, int,   \
-                                  uint32_t*, cudaStream_t, const int*, int);                            \
+                                  uint32_t*, cudaStream_t, const int*, int, int, int);                  \
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
-  template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t);
+  template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t,   \
+                                int64_t);
 #if MPG_WIDE
 #ifdef MPG_WIDE_L  // one wide limb count per translation unit (compile time)
 MPG_INST(MPG_WIDE_L)

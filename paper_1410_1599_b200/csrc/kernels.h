@@ -73,11 +73,13 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 // Children products (7 per parent, hm x hn) -> parent C (rows x cols, stripped).
 // Optional trace output of Winograd's T1/T2 (2 x hm x hn per parent) when t_out != nullptr.
 // rowlist (device, optional): only these child rows [0, hm) are combined (and the parent rows
-// they produce written) -- the row-owned combine of the multi-GPU path.
+// they produce written) -- the row-owned combine of the multi-GPU path.  [cc0, cc0 + ncc): only
+// these child columns (ncc < 0: to the end), i.e. parent columns c and c + hc for each -- the
+// column split of the LU look-ahead (L <= 32).
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st,
-                    const int* rowlist = nullptr, int nrows = 0);
+                    const int* rowlist = nullptr, int nrows = 0, int cc0 = 0, int ncc = -1);
 
 // copy a (rows x cols) window with leading dims (records) -- used by LU
 template <int L>
@@ -143,10 +145,11 @@ void launch_lu_solve(const uint32_t* f, int64_t n, const int64_t* piv_dev, const
                      uint32_t* x, uint32_t* scratch, int sh, uint32_t* err, int64_t* zp,
                      int exact, int64_t nrhs, cudaStream_t st);
 
-// C(view, ldc) = RN(C - T) for a dense rows x cols T (LU Schur subtraction)
+// C(view, ldc) = RN(C - T) for a rows x cols T with leading dimension ldt (< 0: dense) --
+// the LU Schur subtraction
 template <int L>
 void launch_sub2d(uint32_t* C, int64_t ldc, const uint32_t* T, int rows, int cols, int sh,
-                  uint32_t* err, cudaStream_t st);
+                  uint32_t* err, cudaStream_t st, int64_t ldt = -1);
 
 // ---- accuracy metrics (metrics.cu), L in {1..32, 64} -----------------------
 // mode 0: outA[t] = rel_error(approx, ref) = RN(|RN(approx - ref)| / |ref|) at the

@@ -122,7 +122,7 @@ class _FastSharded:
                                                self.up, self.shard.lo, self.shard.hi,
                                                C.c_void_p(self.local.data_ptr()), C.byref(st)))
         _streams_join(h)
-        dist.all_gather_into_tensor(self.all, self.local, group=self.group)
+        all_gather_rows(self.all, self.local, self.group)
         _streams_join(h)
         st2 = _L.MpgpuStats()
         _raise(h, _L.lib.mpgpu_fast_combine(h, self.algo, self.n_min, self.l, self.up,
@@ -262,7 +262,7 @@ class _FastRowOwned:
                                                C.c_void_p(self.local.data_ptr()), C.byref(st)))
         self._copies(self.pack, self.send, self.local)
         _streams_join(h)
-        dist.all_to_all_single(self.recv, self.send, group=self.group)
+        all_to_all_rows(self.recv, self.send, self.group)
         _streams_join(h)
         self._copies(self.unpack, self.full, self.recv)
         st2 = _L.MpgpuStats()
@@ -274,6 +274,33 @@ class _FastRowOwned:
         s.launches += st2.launches
         s.mul, s.addsub = _count(self.algo, self.da, self.db, self.n_min)
         return s
+
+
+def _staged(group) -> bool:
+    """gloo cannot move CUDA tensors: stage the exchange through host memory (the CPU test of
+    the real runners: 2 processes sharing one GPU, gloo over 127.0.0.1)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def all_to_all_rows(recv, send, group):
+    import torch.distributed as dist
+    if _staged(group):
+        r = recv.new_zeros(recv.shape, device="cpu")
+        dist.all_to_all_single(r, send.cpu(), group=group)
+        recv.copy_(r)
+    else:
+        dist.all_to_all_single(recv, send, group=group)
+
+
+def all_gather_rows(out, local, group):
+    import torch.distributed as dist
+    if _staged(group):
+        o = out.new_zeros(out.shape, device="cpu")
+        dist.all_gather_into_tensor(o, local.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, local, group=group)
 
 
 def _streams_join(h):
@@ -324,7 +351,7 @@ class _RowSharded:
             _raise(h, _L.lib.mpgpu_gemm(h, self.algo, self.param, C.byref(av), C.byref(self.db.m), C.byref(cv),
                                         C.byref(st)))
         _streams_join(h)
-        dist.all_gather_into_tensor(self.all, self.local.clone(), group=self.group)
+        all_gather_rows(self.all, self.local.clone(), self.group)
         _streams_join(h)
         # assemble C (rows beyond m are padding)
         nbytes = self.dc.rows() * self.words_per_row * 4

@@ -43,3 +43,4 @@ def P():
 def O():
     from oracle import oracle as O
     return O
+collect_ignore = ["_shard_worker.py"]

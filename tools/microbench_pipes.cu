@@ -16,6 +16,7 @@ template <int OP>
 __global__ void kern(uint32_t seed, uint32_t* out, long long* cyc) {
   uint32_t x[CH], y = seed * 2654435761u + threadIdx.x, z = seed ^ 0x9e3779b9u;
   uint64_t w[CH];
+  const uint64_t zz = ((uint64_t)z << 32) | (seed * 977u);
   uint32_t v[CH];
   double d[CH];
 #pragma unroll
@@ -28,7 +29,9 @@ __global__ void kern(uint32_t seed, uint32_t* out, long long* cyc) {
     for (int c = 0; c < CH; ++c) {
       if (OP == 0) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
       if (OP == 1) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
-      if (OP == 2) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[c]) : "r"(x[c]), "r"(y));
+      // loop-carried multiplier (the low word of the running value): nothing to hoist
+      if (OP == 2)
+        asm volatile("{.reg .u32 t; cvt.u32.u64 t, %0; mad.wide.u32 %0, t, %1, %2;}" : "+l"(w[c]) : "r"(y), "l"(zz));
       if (OP == 3) asm volatile("add.u32 %0, %0, %1; add.u32 %0, %0, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
       if (OP == 4) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[c]) : "r"(y), "r"(z));
       if (OP == 5) asm volatile("shf.l.wrap.b32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(y), "r"(z));
@@ -45,7 +48,7 @@ __global__ void kern(uint32_t seed, uint32_t* out, long long* cyc) {
   long long t1 = clock64();
   uint32_t acc = 0;
 #pragma unroll
-  for (int c = 0; c < CH; ++c) acc ^= x[c] ^ v[c] ^ (uint32_t)w[c] ^ (uint32_t)(uint64_t)d[c];
+  for (int c = 0; c < CH; ++c) acc ^= x[c] ^ v[c] ^ (uint32_t)w[c] ^ (uint32_t)(w[c] >> 32) ^ (uint32_t)(uint64_t)d[c];
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
@@ -168,7 +171,7 @@ int main() {
   const int T = 256, B = 4;
   run(kern<0>, "IMAD (mad.lo.u32)", CH, ITERS, T, B);
   run(kern<1>, "IMAD.HI (mad.hi.u32)", CH, ITERS, T, B);
-  run(kern<2>, "IMAD.WIDE.U32 (mad.wide.u32)", CH, ITERS, T, B);
+  run(kern<2>, "IMAD.WIDE.U32 (mad.wide.u32, loop-carried; 1 op = 1 instruction = 2 IMAD-eq)", CH, ITERS, T, B);
   run(kern<3>, "IADD (2 add.u32 -> IADD3?)", 2 * CH, ITERS, T, B);
   run(kern<4>, "LOP3", CH, ITERS, T, B);
   run(kern<5>, "SHF", CH, ITERS, T, B);

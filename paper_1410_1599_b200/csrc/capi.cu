@@ -32,6 +32,9 @@ struct mpgpu_handle {
   std::string last_error;
   cudaStream_t aux = nullptr;  // second stream of mpgpu_gemm_host (B's upload), lazily created
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // LU look-ahead: the next panel runs on a high-priority stream beside the Schur update
+  cudaStream_t hi = nullptr;
+  cudaEvent_t ev_la = nullptr, ev_lp = nullptr;
 };
 
 namespace {
@@ -1049,6 +1052,12 @@ void mpgpu_destroy(mpgpu_handle* h) {
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_b) cudaEventDestroy(h->ev_b);
+  if (h->hi) {
+    cudaStreamSynchronize(h->hi);
+    cudaStreamDestroy(h->hi);
+  }
+  if (h->ev_la) cudaEventDestroy(h->ev_la);
+  if (h->ev_lp) cudaEventDestroy(h->ev_lp);
   delete h;
 }
 
@@ -1440,6 +1449,214 @@ int mpgpu_fast_mul_trace(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_m
   return check_err(h);
 }
 
+}  // extern "C"
+
+namespace {
+// ---------------------------------------------------------------------------
+// LU look-ahead: the Schur update A22 = RN(A22 - L21 U12) (blocklu.hpp:88-101, 138-141) in two
+// column parts -- part A: columns [0, w) of A22 (the next panel), part B: the rest.  Column
+// slices of the Strassen / Winograd recursion are closed: a child column c feeds only parent
+// columns c and c + hc (post-additions are elementwise per quadrant), and the leaves are plain
+// products whose columns are independent, so computing the leaves' first w columns, the
+// post-additions of child columns [0, w) at every level and then the remainder performs, per
+// element, exactly the unsplit operation sequence: bit-identical results.  Between the parts
+// the caller factors the next panel on another stream (it reads and writes only columns the
+// part-A update finished, while part B writes only the columns beyond).
+// ---------------------------------------------------------------------------
+template <int L>
+struct SchurSplit {
+  std::vector<Level> lv;
+  int d = 0;
+  int64_t nodes = 1;  // leaves
+  std::vector<DevBuf> opA, opB, prod;
+  DevBuf top;
+};
+
+// true if columns [0, w) can be split off: w within every level's child width (leaf columns)
+bool schur_split_ok(int kernel, int64_t rest, int64_t K, int64_t n_min, int64_t w) {
+  if (w <= 0 || w >= rest) return false;
+  if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) return true;
+  const std::vector<Level> lv = plan_levels(rest, K, rest, n_min);
+  return w <= lv.back().n;
+}
+
+// part A (on h->stream): everything for columns [0, w) of a22 (including all pre-additions)
+template <int L>
+int schur_part_a(mpgpu_handle* h, SchurSplit<L>& S_, int kernel, int64_t n_min, const uint32_t* l21,
+                 const uint32_t* u12, uint32_t* a22, int64_t ld, int64_t rest, int64_t K, int64_t w, int sh,
+                 mpgpu_stats* stats) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK ||
+      (S_.lv = plan_levels(rest, K, rest, n_min), S_.d = (int)S_.lv.size() - 1) == 0) {
+    S_.d = 0;
+    const int alg = (kernel == MPGPU_BLOCK) ? MPGPU_BLOCK : MPGPU_SIMPLE;
+    return run_gemm<L>(h, alg, kernel == MPGPU_BLOCK ? n_min : 0, l21, ld, u12, ld, a22, ld, rest, K, w, sh, stats,
+                       1);
+  }
+  const std::vector<Level>& lv = S_.lv;
+  const int d = S_.d;
+  Timer total(stats != nullptr, st);
+  int launches = 0;
+  DevBuf a0, b0;  // dense level-0 operands
+  CUDA_TRY(h, a0.alloc(h, sizeof(uint32_t) * S * rest * K));
+  CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * K * rest));
+  mpg::launch_copy2d<L>(l21, ld, a0.u32(), K, (int)rest, (int)K, st);
+  mpg::launch_copy2d<L>(u12, ld, b0.u32(), rest, (int)K, (int)rest, st);
+  launches += 2;
+  std::vector<DevBuf>(d + 1).swap(S_.opA);  // (DevBuf is not movable: no resize)
+  std::vector<DevBuf>(d + 1).swap(S_.opB);
+  std::vector<DevBuf>(d + 1).swap(S_.prod);
+  {
+    Timer tpre(stats != nullptr, st);
+    int64_t nd = 1;
+    for (int lev = 0; lev < d; ++lev, nd *= 7) {
+      const Level& P = lv[lev];
+      const Level& Q = lv[lev + 1];
+      CUDA_TRY(h, S_.opA[lev + 1].alloc(h, sizeof(uint32_t) * S * nd * 7 * Q.m * Q.l));
+      CUDA_TRY(h, S_.opB[lev + 1].alloc(h, sizeof(uint32_t) * S * nd * 7 * Q.l * Q.n));
+      mpg::launch_preadd<L>(kernel, 0, lev == 0 ? a0.u32() : S_.opA[lev].u32(), nd, (int)P.m, (int)P.l,
+                            S_.opA[lev + 1].u32(), sh, h->d_err, st);
+      mpg::launch_preadd<L>(kernel, 1, lev == 0 ? b0.u32() : S_.opB[lev].u32(), nd, (int)P.l, (int)P.n,
+                            S_.opB[lev + 1].u32(), sh, h->d_err, st);
+      launches += 2;
+      if (lev > 0) {
+        S_.opA[lev].release();
+        S_.opB[lev].release();
+      }
+    }
+    S_.nodes = nd;
+    if (stats) tpre.stop(&stats->preadd_ms);
+  }
+  a0.release();
+  b0.release();
+  const Level& D = lv[d];
+  CUDA_TRY(h, S_.prod[d].alloc(h, sizeof(uint32_t) * S * S_.nodes * D.m * D.n));
+  auto leaf_cols = [&](int64_t c0, int64_t cw) {
+    mpg::GemmArgs g{};
+    g.A = S_.opA[d].u32();
+    g.B = S_.opB[d].u32() + c0 * S;
+    g.C = S_.prod[d].u32() + c0 * S;
+    g.strideA = D.m * D.l;
+    g.strideB = D.l * D.n;
+    g.strideC = D.m * D.n;
+    g.lda = D.l;
+    g.ldb = D.n;
+    g.ldc = D.n;
+    g.m = (int)D.m;
+    g.l = (int)D.l;
+    g.n = (int)cw;
+    g.kb = (int)D.l;
+    g.batch = (int)S_.nodes;
+    g.sh = sh;
+    g.err = h->d_err;
+    mpg::launch_gemm<L>(g, st);
+  };
+  {
+    Timer tl(stats != nullptr, st);
+    leaf_cols(0, w);
+    ++launches;
+    if (stats) {
+      tl.stop(&stats->leaf_ms);
+      stats->leaf_madds = (uint64_t)S_.nodes * D.m * D.l * w;
+    }
+  }
+  Timer tpost(stats != nullptr, st);
+  int64_t nd = S_.nodes;
+  for (int lev = d - 1; lev >= 0; --lev) {
+    nd /= 7;
+    const Level& P = lv[lev];
+    CUDA_TRY(h, S_.prod[lev].alloc(h, sizeof(uint32_t) * S * nd * P.m * P.n));
+    mpg::launch_postadd<L>(kernel, S_.prod[lev + 1].u32(), nd, (int)P.m, (int)P.n, S_.prod[lev].u32(), nullptr, sh,
+                           h->d_err, st, nullptr, 0, 0, (int)w);
+    ++launches;
+  }
+  mpg::launch_sub2d<L>(a22, ld, S_.prod[0].u32(), (int)rest, (int)w, sh, h->d_err, st, rest);
+  ++launches;
+  if (stats) {
+    tpost.stop(&stats->postadd_ms);
+    total.stop(&stats->device_ms);
+    stats->launches = launches;
+    stats->depth = d;
+  }
+  return MPGPU_OK;
+}
+
+// part B (on h->stream, after part A): columns [w, rest) of a22; releases the buffers
+template <int L>
+int schur_part_b(mpgpu_handle* h, SchurSplit<L>& S_, int kernel, int64_t n_min, const uint32_t* l21,
+                 const uint32_t* u12, uint32_t* a22, int64_t ld, int64_t rest, int64_t K, int64_t w, int sh,
+                 mpgpu_stats* stats) {
+  constexpr int S = rec_stride(L);
+  cudaStream_t st = h->stream;
+  if (S_.d == 0) {
+    const int alg = (kernel == MPGPU_BLOCK) ? MPGPU_BLOCK : MPGPU_SIMPLE;
+    return run_gemm<L>(h, alg, kernel == MPGPU_BLOCK ? n_min : 0, l21, ld, u12 + w * S, ld, a22 + w * S, ld, rest,
+                       K, rest - w, sh, stats, 1);
+  }
+  const std::vector<Level>& lv = S_.lv;
+  const int d = S_.d;
+  const Level& D = lv[d];
+  Timer total(stats != nullptr, st);
+  int launches = 0;
+  {
+    Timer tl(stats != nullptr, st);
+    if (D.n > w) {
+      mpg::GemmArgs g{};
+      g.A = S_.opA[d].u32();
+      g.B = S_.opB[d].u32() + w * S;
+      g.C = S_.prod[d].u32() + w * S;
+      g.strideA = D.m * D.l;
+      g.strideB = D.l * D.n;
+      g.strideC = D.m * D.n;
+      g.lda = D.l;
+      g.ldb = D.n;
+      g.ldc = D.n;
+      g.m = (int)D.m;
+      g.l = (int)D.l;
+      g.n = (int)(D.n - w);
+      g.kb = (int)D.l;
+      g.batch = (int)S_.nodes;
+      g.sh = sh;
+      g.err = h->d_err;
+      mpg::launch_gemm<L>(g, st);
+      ++launches;
+    }
+    if (stats) {
+      tl.stop(&stats->leaf_ms);
+      stats->leaf_madds = (uint64_t)S_.nodes * D.m * D.l * (D.n - w);
+    }
+  }
+  S_.opA[d].release();
+  S_.opB[d].release();
+  Timer tpost(stats != nullptr, st);
+  int64_t nd = S_.nodes;
+  for (int lev = d - 1; lev >= 0; --lev) {
+    nd /= 7;
+    const Level& P = lv[lev];
+    const int hc = (int)lv[lev + 1].n;
+    if (hc > w)
+      mpg::launch_postadd<L>(kernel, S_.prod[lev + 1].u32(), nd, (int)P.m, (int)P.n, S_.prod[lev].u32(), nullptr,
+                             sh, h->d_err, st, nullptr, 0, (int)w, hc - (int)w);
+    ++launches;
+    S_.prod[lev + 1].release();
+  }
+  mpg::launch_sub2d<L>(a22 + w * S, ld, S_.prod[0].u32() + w * S, (int)rest, (int)(rest - w), sh, h->d_err, st,
+                       rest);
+  ++launches;
+  S_.prod[0].release();
+  if (stats) {
+    tpost.stop(&stats->postadd_ms);
+    total.stop(&stats->device_ms);
+    stats->launches = launches;
+    stats->depth = d;
+  }
+  return MPGPU_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min, int pivoting,
                      int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats) {
   TimerGuard timer_guard;
@@ -1489,33 +1706,70 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       pc.cnt = reinterpret_cast<int*>(pc.idx + cap);
       pc.cap = cap;
     }
-    auto panel = [&](int64_t p, int64_t k) {
-      // one cooperative launch per panel (grid barriers instead of kernel boundaries:
-      // 1 per column pivot-free, 2 with pivoting); per-column kernels otherwise
+    // the panel factorisation (lu_inplace + trsm_upper_right_inplace over the tall panel, with the
+    // interchanges inside the panel columns) on stream `ps`; grid_cap > 0 bounds the cooperative grid
+    // (the look-ahead leaves the other SMs to the Schur update running beside it)
+    auto panel_factor = [&](int64_t p, int64_t k, cudaStream_t ps, int grid_cap) {
       if (coop && (!pivoting || coop_piv) &&
           mpg::launch_lu_panel_coop<L>(a, n, p, k, n, pivoting, h->d_piv, zp, sh, static_cast<uint64_t*>(cand.p),
                                        reinterpret_cast<int64_t*>(static_cast<uint64_t*>(cand.p) + kMaxGrid),
-                                       kMaxGrid, st) == 0) {
-        if (pivoting) mpg::launch_laswp<L>(a, n, p, k, h->d_piv, zp, st);
+                                       grid_cap > 0 ? grid_cap : kMaxGrid, ps) == 0)
         return;
-      }
       int64_t ncand = 0;  // candidates written by the previous step (0: scan the column)
       for (int64_t d = p; d < p + k; ++d) {
-        if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, pc, ncand, p, p + k, st);
-        ncand = mpg::launch_lu_step<L>(a, n, d, n, p + k, sh, h->d_err, pivoting ? pc : mpg::PivotCands{}, st);
+        if (pivoting) mpg::launch_pivot<L>(a, n, d, n, h->d_piv, zp, pc, ncand, p, p + k, ps);
+        ncand = mpg::launch_lu_step<L>(a, n, d, n, p + k, sh, h->d_err, pivoting ? pc : mpg::PivotCands{}, ps);
       }
+    };
+    // the panel's interchanges applied to the other columns (after every writer of them)
+    auto panel_swap = [&](int64_t p, int64_t k) {
       if (pivoting) mpg::launch_laswp<L>(a, n, p, k, h->d_piv, zp, st);
     };
+    // look-ahead (default on; MPGPU_LU_LOOKAHEAD=0 disables): part A of the Schur update (the next
+    // panel's columns), then the next panel on the high-priority stream beside part B
+    static const bool la_env = [] {
+      const char* e = std::getenv("MPGPU_LU_LOOKAHEAD");
+      return !(e && e[0] == '0');
+    }();
+    const int la_grid = [] {
+      const char* e = std::getenv("MPGPU_LU_LA_GRID");
+      return e ? std::atoi(e) : 32;  // measured: 16 54.2, 32 52.1, 64 53.4, 148 58.3 ms (n=2048, K=64)
+    }();
+    const bool lookahead = la_env && L <= 32;
+    if (lookahead && !h->hi) {
+      int lo = 0, hi_pr = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi_pr);
+      CUDA_TRY(h, cudaStreamCreateWithPriority(&h->hi, cudaStreamNonBlocking, hi_pr));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_la, cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_lp, cudaEventDisableTiming));
+    }
+    bool factored = false;  // the panel at `off` was already factored by the look-ahead
     while (n - off > K) {
       const int64_t rest = n - off - K;
-      panel(off, K);
+      if (!factored) panel_factor(off, K, st, 0);
+      panel_swap(off, K);
       mpg::launch_trsm_l_panel<L>(a, n, off, K, off + K, rest, sh, st);
       const uint32_t* l21 = a + ((off + K) * n + off) * S;
       const uint32_t* u12 = a + (off * n + off + K) * S;
       uint32_t* a22 = a + ((off + K) * n + off + K) * S;
       panel_stats.emplace_back();
       mpgpu_stats& ss = panel_stats.back();  // deque: stable address until the final flush
-      if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) {
+      factored = false;
+      if (lookahead && rest > K && schur_split_ok(kernel, rest, K, n_min, K)) {
+        panel_stats.emplace_back();
+        mpgpu_stats& sb = panel_stats.back();
+        SchurSplit<L> sp;
+        int r = schur_part_a<L>(h, sp, kernel, n_min, l21, u12, a22, n, rest, K, K, sh, stats ? &ss : nullptr);
+        if (r) return r;
+        CUDA_TRY(h, cudaEventRecord(h->ev_la, st));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->hi, h->ev_la, 0));
+        panel_factor(off + K, K, h->hi, la_grid);
+        CUDA_TRY(h, cudaEventRecord(h->ev_lp, h->hi));
+        r = schur_part_b<L>(h, sp, kernel, n_min, l21, u12, a22, n, rest, K, K, sh, stats ? &sb : nullptr);
+        if (r) return r;
+        CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_lp, 0));
+        factored = true;
+      } else if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) {
         int r = run_gemm<L>(h, kernel, n_min, l21, n, u12, n, a22, n, rest, K, rest, sh, stats ? &ss : nullptr, 1);
         if (r) return r;
       } else {
@@ -1534,7 +1788,8 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       }
       off += K;
     }
-    panel(off, n - off);
+    if (!factored) panel_factor(off, n - off, st, 0);
+    panel_swap(off, n - off);
     return 0;
   });
   if (stats) {

@@ -96,10 +96,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
 #define MPG_TILE_ALT_DEN 100
 #endif
 
-#ifndef MPG_PIPE2
-#define MPG_PIPE2 0  // software-pipelined leaf (product k with accumulate k-1): A/B variant
-#endif
-
 #ifndef MPG_NZ_SPLIT
 #define MPG_NZ_SPLIT 1  // measured: -2.3 % leaf time at 256 bits, -1 % at 512
 #endif
@@ -237,12 +233,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     mp_zero(acc[u], 1u);
     mp_zero(pacc[u], 1u);
   }
-  // PIPE: the rounded product waiting to be accumulated (-0 first: RN(-0 + -0) = -0 and
-  // RN(-0 + t0) = t0, so the pipeline's first two accumulates leave pacc = t0 exactly)
-  constexpr bool PIPE = MPG_PIPE2 && !FOLD && U == 1 && L >= 4 && L <= 16;
-  MP<L> tpend[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) mp_zero(tpend[u], 1u);
+
   int next_b = g.kb;  // k at which the next Block k-tile starts
 
   if (tid == 0) {
@@ -287,20 +278,6 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
           const int32_t ae = A_STREAM ? (int32_t)ar[L] : a.e;
           const uint32_t as = A_STREAM ? ar[L + 1] : a.s;
           auto a_at = [&](int q) { return A_STREAM ? ar[q] : a.m[q]; };
-          if constexpr (PIPE) {
-            // software pipeline: the product of step k (FMA-heavy) and the accumulate of step
-            // k-1 (ALU-heavy) in one branch-free block, the rare cases redone exactly
-            MP<L> tn, an;
-            const bool okm = mp_mul_fast<L>(a_at, ae, as, b, g.sh, tn);
-            const bool oka = mp_add_fast<L>(pacc[u], tpend[u], g.sh, an);
-            if (!(okm & oka)) {
-              if (!okm) mp_mul_g<L>(a_at, ae, as, b, g.sh, tn);
-              if (!oka) mp_add<L>(pacc[u], tpend[u], 0u, g.sh, an);
-            }
-            pacc[u] = an;
-            tpend[u] = tn;
-            continue;
-          }
 #if MPG_NZ_SPLIT
           // one zero test for the whole multiply-add: the product of nonzero operands is
           // nonzero, so with a nonzero accumulator neither primitive needs its own
@@ -321,10 +298,6 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     __syncthreads();
   }
   if (!active) return;
-  if constexpr (PIPE) {  // drain the pipeline: the last product
-#pragma unroll
-    for (int u = 0; u < U; ++u) mp_add<L>(pacc[u], tpend[u], 0u, g.sh, pacc[u]);
-  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int j = j0 + tx + u * TN;

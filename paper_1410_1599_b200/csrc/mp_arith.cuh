@@ -617,90 +617,6 @@ MPG_UNROLL
   z.e = e;
 }
 
-// ---------------------------------------------------------------------------
-// Branch-free common paths of mp_mul / mp_add for the software-pipelined GEMM leaf
-// (gemm.cu, MPG_PIPE2): no branches, so the compiler can interleave the FMA-heavy limb
-// products of step k+1 with the ALU-heavy alignment / normalisation / rounding of step k.
-// Each returns false when its operands leave the common case (zeros, p != 32 L, a short
-// product too close to a rounding boundary, an exponent gap >= 32, |y| > |x| at equal
-// exponents, >= 32 bits of cancellation); the caller then recomputes with mp_mul_g /
-// mp_add.  When true, the result is exactly mp_mul_g's / mp_add's.
-// ---------------------------------------------------------------------------
-template <int L, class AG>
-__device__ __forceinline__ bool mp_mul_fast(AG a_at, int32_t xe, uint32_t xs, const MP<L>& y, int sh, MP<L>& z) {
-  static_assert(L >= 3 && L <= 32, "short-product path");
-  uint32_t P[2 * L];
-  mul_high_g<L>(a_at, y.m, P);
-  const uint32_t t1 = (P[2 * L - 1] >> 31) ^ 1u;
-  const uint32_t gt = __funnelshift_l(P[L - 2], P[L - 1], t1);
-  const bool down = gt < 0x80000000u - 2u * L;
-  const bool up = gt > 0x80000000u && gt < 0xFFFFFFFFu - 2u * L;
-MPG_UNROLL
-  for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], t1);
-  const uint32_t c = add_word<L>(z.m, up ? 1u : 0u);
-  z.m[L - 1] |= c << 31;  // all ones rounded up: 1000...0 (the other limbs wrapped to 0)
-  z.e = xe + y.e - (int32_t)t1 + (int32_t)c;
-  z.s = xs ^ y.s;
-  return (down | up) & (sh == 0) & (xe != EXP_ZERO) & (y.e != EXP_ZERO);
-}
-
-template <int L>
-__device__ __forceinline__ bool mp_add_fast(const MP<L>& x, const MP<L>& y_in, int sh, MP<L>& z) {
-  constexpr int W = L + 1;
-  const uint32_t ys = y_in.s;
-  const bool swp = y_in.e > x.e;
-  uint32_t A[W], B[W];
-  A[0] = 0;
-  B[0] = 0;
-MPG_UNROLL
-  for (int k = 0; k < L; ++k) {
-    A[k + 1] = swp ? y_in.m[k] : x.m[k];
-    B[k + 1] = swp ? x.m[k] : y_in.m[k];
-  }
-  const int32_t ebig = swp ? y_in.e : x.e;
-  const uint32_t d = (uint32_t)(swp ? y_in.e - x.e : x.e - y_in.e);
-  const uint32_t sbig = swp ? ys : x.s;
-  const uint32_t sub = sbig ^ (swp ? x.s : ys);
-  const uint32_t dd = d & 31u;
-MPG_UNROLL
-  for (int k = 0; k < W - 1; ++k) B[k] = __funnelshift_r(B[k], B[k + 1], dd);
-  B[W - 1] >>= dd;
-  const uint32_t mask = 0u - sub;
-  uint32_t R[W], cout;
-  {
-    const uint32_t m1 = 1u - 2u * sub;  // B ^ mask as an IMAD (FMA pipe), as in mp_add
-MPG_UNROLL
-    for (int k = 0; k < W; ++k) B[k] = B[k] * m1 + mask;
-    asm("add.cc.u32 %0, %1, %2;" : "=r"(R[0]) : "r"(B[0]), "r"(sub));  // A[0] == 0, carry-in 1 - sticky = 1
-MPG_UNROLL
-    for (int k = 1; k < W; ++k) asm("addc.cc.u32 %0, %1, %2;" : "=r"(R[k]) : "r"(A[k]), "r"(B[k]));
-    asm("addc.u32 %0, 0, 0;" : "=r"(cout));
-  }
-  const bool ok = (d < 32u) & !(sub & ((cout ^ 1u) | (R[W - 1] == 0))) & (x.e != EXP_ZERO) &
-                  (y_in.e != EXP_ZERO) & (sh == 0);
-  int32_t e = ebig;
-  const uint32_t c1 = cout & (sub ^ 1u);
-  uint32_t st = R[0] & c1;
-MPG_UNROLL
-  for (int k = 0; k < W - 1; ++k) R[k] = __funnelshift_r(R[k], R[k + 1], c1);
-  R[W - 1] = (R[W - 1] >> c1) | (c1 << 31);
-  const uint32_t lz = __clz(R[W - 1]) & 31u;
-MPG_UNROLL
-  for (int k = W - 1; k > 0; --k) R[k] = __funnelshift_l(R[k - 1], R[k], lz);
-  R[0] <<= lz;
-  e += (int32_t)c1 - (int32_t)lz;
-  // round to nearest even at p = 32 L: guard limb R[0], sticky st
-  const uint32_t g = R[0];
-  const uint32_t upb = (g >> 31) & ((((g << 1) | st) != 0) | (R[1] & 1u));
-MPG_UNROLL
-  for (int k = 0; k < L; ++k) z.m[k] = R[k + 1];
-  const uint32_t c = add_word<L>(z.m, upb);
-  z.m[L - 1] |= c << 31;
-  z.e = e + (int32_t)c;
-  z.s = sbig;
-  return ok;
-}
-
 template <int L>
 __device__ __forceinline__ void mp_zero(MP<L>& z, uint32_t s = 0) {
 MPG_UNROLL

@@ -209,6 +209,14 @@ int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out
 int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
                       int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products,
                       mpgpu_stats* stats);
+/* The same, with the exchange fused into the producing kernel: row r of node u (u = 0 ..
+ * node_hi - node_lo - 1) is written to row_dst[r] + u * (rows * cols) records, where row_dst
+ * (a DEVICE array of node-row count 64-bit addresses) may point into other GPUs' memory (peer
+ * access over NVLink): the leaf GEMM's (or last local post-addition's) epilogue stores every
+ * product row straight into the buffer of the device that owns it.  Precisions <= 1024 bits. */
+int mpgpu_fast_leaves_rows(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                           int up_levels, int64_t node_lo, int64_t node_hi, const uint64_t* row_dst,
+                           mpgpu_stats* stats);
 int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
                        const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats);
 /* Row-owned combine: node_products holds (at least) rows [row_lo, row_hi) of every

@@ -66,6 +66,8 @@ _SIGS = {
     "mpgpu_fast_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p]),
     "mpgpu_fast_leaves": (C.c_int, [vp, C.c_int, C.c_int64, MatP, MatP, C.c_int, C.c_int64, C.c_int64, vp,
                                     StatsP]),
+    "mpgpu_fast_leaves_rows": (C.c_int, [vp, C.c_int, C.c_int64, MatP, MatP, C.c_int, C.c_int64, C.c_int64, vp,
+                                         StatsP]),
     "mpgpu_fast_combine": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, MatP, StatsP]),
     "mpgpu_fast_combine_rows": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, C.c_int64, C.c_int64,
                                           MatP, StatsP]),

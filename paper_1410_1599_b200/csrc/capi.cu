@@ -639,7 +639,7 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
 template <int L>
 int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A, int64_t lda, const uint32_t* B,
                     int64_t ldb, int64_t m, int64_t l, int64_t n, int64_t ulo, int64_t uhi, int up_levels,
-                    uint32_t* out, int sh, mpgpu_stats* stats) {
+                    uint32_t* out, int sh, mpgpu_stats* stats, const uint64_t* rowtab = nullptr) {
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   const bool timing = stats != nullptr;
@@ -710,6 +710,7 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
     DevBuf leafbuf;
     if (up_levels == 0) {
       g.C = out;
+      g.rowtab = rowtab;  // (fused exchange: rows straight to their owners)
     } else {
       CUDA_TRY(h, leafbuf.alloc(h, sizeof(uint32_t) * S * (hi - lo) * D.m * D.n));
       g.C = leafbuf.u32();
@@ -751,7 +752,8 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
         CUDA_TRY(h, next.alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
         dst = next.u32();
       }
-      mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st);
+      mpg::launch_postadd<L>(algo, cur, nodes, (int)P.m, (int)P.n, dst, nullptr, sh, h->d_err, st, nullptr, 0, 0,
+                             -1, k == up_levels - 1 ? rowtab : nullptr);
       ++launches;
       if (k == 0) leafbuf.release();
       cur_owner.release();
@@ -1906,10 +1908,34 @@ int mpgpu_fast_plan(int64_t m, int64_t l, int64_t n, int64_t n_min, int64_t* out
   return MPGPU_OK;
 }
 
+namespace {
+int fast_leaves_impl(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                     int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products,
+                     const uint64_t* rowtab, mpgpu_stats* stats);
+}
+
 int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
                       int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products, mpgpu_stats* stats) {
+  if (!node_products) return MPGPU_ERR_DOMAIN;
+  return fast_leaves_impl(h, algo, n_min, A, B, up_levels, node_lo, node_hi, node_products, nullptr, stats);
+}
+
+int mpgpu_fast_leaves_rows(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                           int up_levels, int64_t node_lo, int64_t node_hi, const uint64_t* row_dst,
+                           mpgpu_stats* stats) {
+  if (!row_dst) return MPGPU_ERR_DOMAIN;
+  if (A && A->nlimbs > 32) return fail(h, MPGPU_ERR_DOMAIN, "row destinations: precisions up to 1024 bits");
+  return fast_leaves_impl(h, algo, n_min, A, B, up_levels, node_lo, node_hi, nullptr, row_dst, stats);
+}
+
+}  // extern "C"
+
+namespace {
+int fast_leaves_impl(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat* A, const mpgpu_mat* B,
+                     int up_levels, int64_t node_lo, int64_t node_hi, uint32_t* node_products,
+                     const uint64_t* rowtab, mpgpu_stats* stats) {
   TimerGuard timer_guard;
-  if (!h || !A || !B || !node_products) return MPGPU_ERR_DOMAIN;
+  if (!h || !A || !B) return MPGPU_ERR_DOMAIN;
   if (int r = compute_range(h, {A, B})) return r;
   if (A->cols != B->rows) return fail(h, MPGPU_ERR_DIMENSION, "inner dimension mismatch");
   if (n_min < 1) return fail(h, MPGPU_ERR_DIMENSION, "n_min must be at least 1");
@@ -1923,11 +1949,15 @@ int mpgpu_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const mpgpu_mat*
   const int sh = 32 * A->nlimbs - A->prec;
   int rc = dispatch_L(A->nlimbs, [&](auto Lc) {
     return run_fast_leaves<decltype(Lc)::value>(h, algo, n_min, A->rec, A->ld, B->rec, B->ld, A->rows, A->cols,
-                                                B->cols, node_lo, node_hi, up_levels, node_products, sh, stats);
+                                                B->cols, node_lo, node_hi, up_levels, node_products, sh, stats,
+                                                rowtab);
   });
   if (rc) return rc;
   return check_err(h);
 }
+}  // namespace
+
+extern "C" {
 
 int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
                        const uint32_t* node_products, mpgpu_mat* C, mpgpu_stats* stats) {

@@ -237,10 +237,12 @@ __global__ void convert_kernel(const uint32_t* __restrict__ src, int ls, int ss,
 
 template <int L>
 __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r, int c, const MP<L>& x,
-                                         uint32_t* err) {
+                                         uint32_t* err, const uint64_t* rowtab = nullptr, int64_t node = 0) {
   if (r < rows && c < cols) {
     if (exp_out_of_range(x.e)) atomicOr(err, ERR_EXP_RANGE);
-    store_rec<L>(P + ((int64_t)r * cols + c) * rec_stride(L), x);
+    uint32_t* dst = rowtab ? reinterpret_cast<uint32_t*>(rowtab[r]) + (node * rows * cols + c) * rec_stride(L)
+                           : P + ((int64_t)r * cols + c) * rec_stride(L);
+    store_rec<L>(dst, x);
   }
 }
 
@@ -248,7 +250,7 @@ template <int L>
 __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
                                int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
                                int sh, uint32_t* err, const int* __restrict__ rowlist, int nrows, int cc0,
-                               int ncc) {
+                               int ncc, const uint64_t* __restrict__ rowtab) {
   constexpr int S = rec_stride(L);
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
   const int64_t per = (int64_t)hr * hc;
@@ -286,7 +288,7 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
         MP<L> m3;
         load_rec<L>(M + 2 * cs, m3);
         mp_add<L>(m2, m3, 0u, sh, u);
-        store_if<L>(P, rows, cols, r, c, u, err);
+        store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
       }
       MP<L> m5;
       load_rec<L>(M + 4 * cs, m5);
@@ -295,16 +297,16 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
         load_rec<L>(M + 5 * cs, m6);
         mp_add<L>(t1, m5, 0u, sh, u);
         mp_add<L>(u, m6, 0u, sh, v);
-        store_if<L>(P, rows, cols, r, c + hc, v, err);
+        store_if<L>(P, rows, cols, r, c + hc, v, err, rowtab, node);
       }
       {
         MP<L> m7;
         load_rec<L>(M + 6 * cs, m7);
         mp_add<L>(t2, m7, 1u, sh, u);
-        store_if<L>(P, rows, cols, r + hr, c, u, err);
+        store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
       }
       mp_add<L>(t2, m5, 0u, sh, u);
-      store_if<L>(P, rows, cols, r + hr, c + hc, u, err);
+      store_if<L>(P, rows, cols, r + hr, c + hc, u, err, rowtab, node);
     } else {
       // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
       MP<L> p1, p4, p5, u, v;
@@ -317,23 +319,23 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
         MP<L> p7;
         load_rec<L>(M + 6 * cs, p7);
         mp_add<L>(v, p7, 0u, sh, u);
-        store_if<L>(P, rows, cols, r, c, u, err);
+        store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
       }
       MP<L> p3;
       load_rec<L>(M + 2 * cs, p3);
       mp_add<L>(p3, p5, 0u, sh, u);
-      store_if<L>(P, rows, cols, r, c + hc, u, err);
+      store_if<L>(P, rows, cols, r, c + hc, u, err, rowtab, node);
       MP<L> p2;
       load_rec<L>(M + 1 * cs, p2);
       mp_add<L>(p2, p4, 0u, sh, u);
-      store_if<L>(P, rows, cols, r + hr, c, u, err);
+      store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
       mp_add<L>(p1, p3, 0u, sh, u);
       mp_add<L>(u, p2, 1u, sh, v);
       {
         MP<L> p6;
         load_rec<L>(M + 5 * cs, p6);
         mp_add<L>(v, p6, 0u, sh, u);
-        store_if<L>(P, rows, cols, r + hr, c + hc, u, err);
+        store_if<L>(P, rows, cols, r + hr, c + hc, u, err, rowtab, node);
       }
     }
   }
@@ -422,13 +424,13 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist,
-                    int nrows, int cc0, int ncc) {
+                    int nrows, int cc0, int ncc, const uint64_t* rowtab) {
   const int hc = (cols + cols % 2) / 2;
   if (ncc < 0) ncc = hc - cc0;
 #if MPG_WIDE
   if constexpr (L > 32)
-    if (wmp::enabled()) {  // (the column split is not used with the wide formats)
-      if (cc0 != 0 || ncc != hc) return;
+    if (wmp::enabled()) {  // (the column split and row tables are not used with the wide formats)
+      if (cc0 != 0 || ncc != hc || rowtab) return;
       return wmp::launch_postadd<L / 32>(algo, children, nodes, rows, cols, parent, t_out, sh, err, st, rowlist,
                                          nrows);
     }
@@ -436,7 +438,7 @@ void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows,
   const int64_t total = (int64_t)(rowlist ? nrows : (rows + rows % 2) / 2) * ncc * nodes;
   if (total <= 0) return;
   postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,
-                                                     err, rowlist, nrows, cc0, ncc);
+                                                     err, rowlist, nrows, cc0, ncc, rowtab);
 }
 template <int L>
 void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
@@ -462,7 +464,7 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_preadd<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int,          \
                                  uint32_t*, cudaStream_t);                                              \
   template void launch_postadd<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, uint32_t*, int,   \
-                                  uint32_t*, cudaStream_t, const int*, int, int, int);                  \
+                                  uint32_t*, cudaStream_t, const int*, int, int, int, const uint64_t*); \
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t,   \

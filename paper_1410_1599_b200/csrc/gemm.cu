@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     } else {
       res = pacc[u];
     }
-    uint32_t* cr = C + ((int64_t)i * g.ldc + j) * S;
+    uint32_t* cr = g.rowtab ? reinterpret_cast<uint32_t*>(g.rowtab[i]) + ((g.batch0 + z) * g.strideC + j) * S
+                            : C + ((int64_t)i * g.ldc + j) * S;
     if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
       MP<L> old;
       load_rec<L>(cr, old);
@@ -333,6 +334,7 @@ void launch_tiles(const GemmArgs& g, cudaStream_t st) {
     gz.A += (int64_t)z0 * g.strideA * S;
     gz.B += (int64_t)z0 * g.strideB * S;
     gz.C += (int64_t)z0 * g.strideC * S;
+    gz.batch0 = g.batch0 + z0;
     dim3 grid((g.n + TN * U - 1) / (TN * U), (g.m + TM - 1) / TM, gz.batch);
     kern<<<grid, TM * TN, smem, st>>>(gz);
   }
@@ -345,7 +347,7 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st) {
     if (wmp::enabled()) return wmp::launch_gemm<L / 32>(g, st);
 #endif
   if constexpr (L == 8 || L == 16 || L == 32) {  // tensor-core leaf (gemm_tc.cu) when MPGPU_GEMM=tc
-    if (gemm_tc_enabled() && launch_gemm_tc<L>(g, st)) return;
+    if (gemm_tc_enabled() && !g.rowtab && launch_gemm_tc<L>(g, st)) return;
   }
   constexpr int TM = GemmCfg<L>::TM, TN = GemmCfg<L>::TN, U = GemmCfg<L>::U;
   if constexpr (U == 1 && TN == 16 && L <= 32) {

@@ -26,6 +26,7 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -298,61 +299,102 @@ int mpgpu_group_gemm_host(mpgpu_group* g, int algo, int64_t param, int32_t prec,
     const std::vector<Range> rr = even_ranges(um, world, &rows_per);
     const int64_t rw = mpgpu_record_words(L);
     const int64_t row_w = un * rw, unit_w = um * row_w;  // 32-bit words
-    std::vector<uint32_t*> local(world, nullptr);
+    std::vector<uint32_t*> local(world, nullptr), fullv(world, nullptr);
+    // fused exchange (default, <= 1024 bits): every device's leaf / last local post-addition
+    // epilogue stores each unit-product row straight into its owner's buffer over NVLink; the
+    // pull variant (MPGPU_GROUP_PULL=1) copies row slices afterwards with cudaMemcpy2DAsync
+    static const bool pull_env = [] {
+      const char* e = std::getenv("MPGPU_GROUP_PULL");
+      return e && e[0] == '1';
+    }();
+    const bool fused = !pull_env && L <= 32;
     auto work = [&](int i) {
       mpgpu_handle* h = g->h[i];
       cudaSetDevice(g->devices[i]);
       cudaStream_t s = static_cast<cudaStream_t>(mpgpu_get_stream(h));
       mpgpu_mat da{}, db{}, dc{};
       uint32_t* full = nullptr;
+      uint64_t* rowtab = nullptr;
       mpgpu_stats s_leaf{}, s_comb{};
+      const Range u = ur[i];
+      const Range r = rr[i];
+      const int64_t hr = r.hi - r.lo;
       int rc = mpgpu_alloc_matrix(h, m, l, prec, &da);
       if (!rc) rc = mpgpu_alloc_matrix(h, l, n, prec, &db);
       if (!rc) rc = mpgpu_upload(h, &da, A.l, A.e, A.s, Lh);
       if (!rc) rc = mpgpu_upload(h, &db, B.l, B.e, B.s, Lh);
-      const Range u = ur[i];
-      if (!rc && u.hi > u.lo) {
+      if (fused) {
+        // the owner's buffer first: every producer needs every owner's address
         cudaSetDevice(g->devices[i]);
-        if (cudaMalloc(&local[i], sizeof(uint32_t) * (size_t)((u.hi - u.lo) * unit_w)) != cudaSuccess) {
+        if (!rc && hr > 0 && cudaMalloc(&fullv[i], sizeof(uint32_t) * (size_t)(units * unit_w)) != cudaSuccess) {
           cudaGetLastError();
           rc = MPGPU_ERR_NOMEM;
         }
-        if (!rc)
-          rc = mpgpu_fast_leaves(h, algo, param, &da, &db, up, u.lo, u.hi, local[i], stats ? &s_leaf : nullptr);
-      }
-      mpgpu_free_matrix(h, &da);
-      mpgpu_free_matrix(h, &db);
-      if (rc) set_fail(i, rc, "leaf shard");
-      bar.wait();  // every device's unit products are complete (mpgpu_fast_leaves is synchronous)
-      const Range r = rr[i];
-      const int64_t hr = r.hi - r.lo;
-      if (!any_failed() && hr > 0) {
-        cudaSetDevice(g->devices[i]);
-        if (cudaMalloc(&full, sizeof(uint32_t) * (size_t)(units * unit_w)) != cudaSuccess) {
-          cudaGetLastError();
-          set_fail(i, MPGPU_ERR_NOMEM, "unit buffer");
-        } else {
-          // pull rows [r.lo, r.hi) of every unit product from the device that made it
-          for (int j = 0; j < world && !rc; ++j) {
-            const Range uj = ur[j];
-            if (uj.hi <= uj.lo) continue;
-            const cudaError_t e = cudaMemcpy2DAsync(
-                full + (uj.lo * um + r.lo) * row_w, sizeof(uint32_t) * unit_w, local[j] + r.lo * row_w,
-                sizeof(uint32_t) * unit_w, sizeof(uint32_t) * hr * row_w, uj.hi - uj.lo, cudaMemcpyDefault, s);
-            if (e != cudaSuccess) {
-              cudaGetLastError();
-              rc = MPGPU_ERR_CUDA;
-            }
+        if (rc) set_fail(i, rc, "unit buffer");
+        bar.wait();  // all owners' buffers exist
+        full = fullv[i];
+        if (!any_failed() && u.hi > u.lo) {
+          // row r of this device's node t lands in owner(r)'s buffer at unit u.lo + t
+          std::vector<uint64_t> tab(um);
+          for (int j = 0; j < world; ++j)
+            for (int64_t rr_ = rr[j].lo; rr_ < rr[j].hi; ++rr_)
+              tab[rr_] = reinterpret_cast<uint64_t>(fullv[j] + (u.lo * um + rr_) * row_w);
+          cudaSetDevice(g->devices[i]);
+          if (cudaMalloc(&rowtab, sizeof(uint64_t) * um) != cudaSuccess ||
+              cudaMemcpy(rowtab, tab.data(), sizeof(uint64_t) * um, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            rc = MPGPU_ERR_CUDA;
           }
-          if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = MPGPU_ERR_CUDA;
-          if (rc) set_fail(i, rc, "peer pull");
+          if (!rc)
+            rc = mpgpu_fast_leaves_rows(h, algo, param, &da, &db, up, u.lo, u.hi, rowtab, stats ? &s_leaf : nullptr);
+          if (rowtab) cudaFree(rowtab);
+          if (rc) set_fail(i, rc, "leaf shard (fused exchange)");
         }
-      }
-      bar.wait();  // every pull is complete: the producers' buffers may go
-      if (local[i]) {
-        cudaSetDevice(g->devices[i]);
-        cudaFree(local[i]);
-        local[i] = nullptr;
+        mpgpu_free_matrix(h, &da);
+        mpgpu_free_matrix(h, &db);
+        bar.wait();  // every product row is in its owner's buffer (the producers synchronised)
+      } else {
+        if (!rc && u.hi > u.lo) {
+          cudaSetDevice(g->devices[i]);
+          if (cudaMalloc(&local[i], sizeof(uint32_t) * (size_t)((u.hi - u.lo) * unit_w)) != cudaSuccess) {
+            cudaGetLastError();
+            rc = MPGPU_ERR_NOMEM;
+          }
+          if (!rc)
+            rc = mpgpu_fast_leaves(h, algo, param, &da, &db, up, u.lo, u.hi, local[i], stats ? &s_leaf : nullptr);
+        }
+        mpgpu_free_matrix(h, &da);
+        mpgpu_free_matrix(h, &db);
+        if (rc) set_fail(i, rc, "leaf shard");
+        bar.wait();  // every device's unit products are complete (mpgpu_fast_leaves is synchronous)
+        if (!any_failed() && hr > 0) {
+          cudaSetDevice(g->devices[i]);
+          if (cudaMalloc(&full, sizeof(uint32_t) * (size_t)(units * unit_w)) != cudaSuccess) {
+            cudaGetLastError();
+            set_fail(i, MPGPU_ERR_NOMEM, "unit buffer");
+          } else {
+            // pull rows [r.lo, r.hi) of every unit product from the device that made it
+            for (int j = 0; j < world && !rc; ++j) {
+              const Range uj = ur[j];
+              if (uj.hi <= uj.lo) continue;
+              const cudaError_t e = cudaMemcpy2DAsync(
+                  full + (uj.lo * um + r.lo) * row_w, sizeof(uint32_t) * unit_w, local[j] + r.lo * row_w,
+                  sizeof(uint32_t) * unit_w, sizeof(uint32_t) * hr * row_w, uj.hi - uj.lo, cudaMemcpyDefault, s);
+              if (e != cudaSuccess) {
+                cudaGetLastError();
+                rc = MPGPU_ERR_CUDA;
+              }
+            }
+            if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = MPGPU_ERR_CUDA;
+            if (rc) set_fail(i, rc, "peer pull");
+          }
+        }
+        bar.wait();  // every pull is complete: the producers' buffers may go
+        if (local[i]) {
+          cudaSetDevice(g->devices[i]);
+          cudaFree(local[i]);
+          local[i] = nullptr;
+        }
       }
       if (!any_failed() && hr > 0) {
         rc = mpgpu_alloc_matrix(h, m, n, prec, &dc);

@@ -38,6 +38,11 @@ struct GemmArgs {
   uint32_t* err;
   // optional LU Schur epilogue: C = RN(C - A*B) in place (blocklu.hpp:138-141)
   int sub_from_c;
+  // optional row destinations (multi-GPU exchange fused into the epilogue): row i of batch
+  // item z goes to rowtab[i] + (batch0 + z) * strideC records -- rowtab[i] may point into
+  // another GPU's memory (peer access), so the products land at their owners as they are made
+  const uint64_t* rowtab;
+  int64_t batch0;
 };
 
 template <int L>
@@ -76,10 +81,13 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 // they produce written) -- the row-owned combine of the multi-GPU path.  [cc0, cc0 + ncc): only
 // these child columns (ncc < 0: to the end), i.e. parent columns c and c + hc for each -- the
 // column split of the LU look-ahead (L <= 32).
+// rowtab (device, optional): parent row r of node t goes to rowtab[r] + t * rows * cols records
+// (the fused multi-GPU exchange, as GemmArgs::rowtab; L <= 32).
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st,
-                    const int* rowlist = nullptr, int nrows = 0, int cc0 = 0, int ncc = -1);
+                    const int* rowlist = nullptr, int nrows = 0, int cc0 = 0, int ncc = -1,
+                    const uint64_t* rowtab = nullptr);
 
 // copy a (rows x cols) window with leading dims (records) -- used by LU
 template <int L>

@@ -68,3 +68,29 @@ def test_group_cfg2_shape(P):
     got = P.Matrix(n, n, ctx)
     P.DeviceGroup([0, 0, 0, 0]).gemm_host(P.Algorithm.winograd, 32, a, b, got, ctx)
     assert P.identical(got, want)
+
+
+@pytest.mark.parametrize("pull", ["0", "1"])
+def test_group_exchange_variants(P, pull, monkeypatch):
+    # fused exchange (epilogue stores rows into their owners' buffers) and the copy-engine pull
+    # are the same bits; MPGPU_GROUP_PULL is read once per process, so run each in a subprocess
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys; sys.path.insert(0, '.')
+        import paper_1410_1599_b200 as P
+        for bits, (m, l, n), nm in ((256, (96, 80, 72), 8), (1024, (40, 36, 44), 5), (128, (130, 70, 90), 9)):
+            ctx = P.PrecisionContext(bits)
+            a, b = P.gen_uniform_full(m, l, 3, ctx), P.gen_uniform_full(l, n, 4, ctx)
+            for algo in ("strassen", "winograd"):
+                want = P.Matrix(m, n, ctx); P.gemm_host(P.Algorithm[algo], nm, a, b, want, ctx)
+                for shards in (2, 3, 5):
+                    got = P.Matrix(m, n, ctx)
+                    P.DeviceGroup([0] * shards).gemm_host(P.Algorithm[algo], nm, a, b, got, ctx)
+                    assert P.identical(got, want), (bits, algo, shards)
+        print("OK")
+    """)
+    import os
+    env = dict(os.environ, MPGPU_GROUP_PULL=pull)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]

@@ -9,11 +9,11 @@ resident operands.  --algo block|strassen|winograd|simple selects the other arms
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): the 7^d leaf products are sharded across ranks (each rank does
-the pre-additions for its own leaves from replicated A and B, no data-path
-collective on the leaf work); one all-to-all moves the unit products' row slices
-to their owners and each rank post-adds its own rows of C (see DESIGN.md
-"Multi-GPU").  Timing: CUDA events around each step
+N > 1 (one process per GPU; started without torchrun, bench.py re-launches itself as N
+ranks): the 7^d leaf products are sharded across ranks (each rank does the pre-additions
+for its own leaves from replicated A and B); the leaf kernel's epilogue stores every
+product row straight into the buffer of the rank that owns it (peer memory over NVLink,
+CUDA IPC) and each rank post-adds its own rows of C.  Timing: CUDA events around each step
 on the launching stream, an L2 flush (256 MiB write) between steps, barrier +
 synchronize on both sides, max over ranks.
 """
@@ -57,10 +57,11 @@ def parse():
                     help="print this rank's (rank, world) as JSON and exit before touching CUDA (launcher test)")
     ap.add_argument("--cfg4", action="store_true", help="also time config 4 (n=4096 @1024) at N=1")
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 leg at N>1")
-    ap.add_argument("--shard", choices=["auto", "gather", "replicas"], default="auto",
-                    help="N>1: auto = leaf shards with one all-to-all and a row-owned combine "
-                         "(Strassen/Winograd) or row shards (Simple/Block) (strong scaling); gather = "
-                         "leaf shards + all-gather + replicated combine; replicas = independent copies (weak)")
+    ap.add_argument("--shard", choices=["auto", "a2a", "gather", "replicas"], default="auto",
+                    help="N>1: auto = leaf shards whose leaf epilogue stores the product rows into their owners' "
+                         "buffers over peer memory (CUDA IPC, NVLink), then a row-owned combine (Strassen/Winograd), "
+                         "or row shards (Simple/Block) (strong scaling); a2a = the same with an NCCL all-to-all; "
+                         "gather = leaf shards + all-gather + replicated combine; replicas = independent copies (weak)")
     return ap.parse_args()
 
 

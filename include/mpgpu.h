@@ -228,6 +228,16 @@ int mpgpu_fast_combine(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int 
 int mpgpu_fast_combine_rows(mpgpu_handle* h, int algo, int64_t n_min, int64_t l, int up_levels,
                             const uint32_t* node_products, int64_t row_lo, int64_t row_hi, mpgpu_mat* C,
                             mpgpu_stats* stats);
+/* Device buffers shared between processes (one process per GPU): plain cudaMalloc memory, its
+ * CUDA IPC handle (MPGPU_IPC_HANDLE_BYTES opaque bytes, exchanged by the caller, e.g. with
+ * torch.distributed), and a peer process's buffer mapped into this one (peer access enabled) --
+ * the destinations of mpgpu_fast_leaves_rows across processes. */
+#define MPGPU_IPC_HANDLE_BYTES 64
+int mpgpu_malloc(mpgpu_handle* h, size_t bytes, void** out);
+int mpgpu_free(mpgpu_handle* h, void* p);
+int mpgpu_ipc_handle(mpgpu_handle* h, void* p, void* handle_out);
+int mpgpu_ipc_open(mpgpu_handle* h, const void* handle, void** out);
+int mpgpu_ipc_close(mpgpu_handle* h, void* p);
 /* device-to-device 2D copy on the handle's stream (packing row slices for the all-to-all) */
 int mpgpu_copy_device_2d(mpgpu_handle* h, void* dst, size_t dpitch, const void* src, size_t spitch,
                          size_t width, size_t height);

@@ -68,6 +68,11 @@ _SIGS = {
                                     StatsP]),
     "mpgpu_fast_leaves_rows": (C.c_int, [vp, C.c_int, C.c_int64, MatP, MatP, C.c_int, C.c_int64, C.c_int64, vp,
                                          StatsP]),
+    "mpgpu_malloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
+    "mpgpu_free": (C.c_int, [vp, vp]),
+    "mpgpu_ipc_handle": (C.c_int, [vp, vp, vp]),
+    "mpgpu_ipc_open": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "mpgpu_ipc_close": (C.c_int, [vp, vp]),
     "mpgpu_fast_combine": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, MatP, StatsP]),
     "mpgpu_fast_combine_rows": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp, C.c_int64, C.c_int64,
                                           MatP, StatsP]),

@@ -2012,6 +2012,53 @@ int mpgpu_copy_device_2d(mpgpu_handle* h, void* dst, size_t dpitch, const void* 
   return MPGPU_OK;
 }
 
+// ---- device memory shared between processes (one process per GPU, peer stores) --------
+int mpgpu_malloc(mpgpu_handle* h, size_t bytes, void** out) {
+  if (!h || !out) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaMalloc(out, bytes < 16 ? 16 : bytes));
+  return MPGPU_OK;
+}
+
+int mpgpu_free(mpgpu_handle* h, void* p) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  if (!p) return MPGPU_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaFree(p));
+  return MPGPU_OK;
+}
+
+int mpgpu_ipc_handle(mpgpu_handle* h, void* p, void* handle_out) {
+  if (!h || !p || !handle_out) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  cudaIpcMemHandle_t ih;
+  CUDA_TRY(h, cudaIpcGetMemHandle(&ih, p));
+  std::memcpy(handle_out, &ih, sizeof ih);
+  return MPGPU_OK;
+}
+
+int mpgpu_ipc_open(mpgpu_handle* h, const void* handle, void** out) {
+  if (!h || !handle || !out) return MPGPU_ERR_DOMAIN;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  cudaIpcMemHandle_t ih;
+  std::memcpy(&ih, handle, sizeof ih);
+  CUDA_TRY(h, cudaIpcOpenMemHandle(out, ih, cudaIpcMemLazyEnablePeerAccess));
+  return MPGPU_OK;
+}
+
+int mpgpu_ipc_close(mpgpu_handle* h, void* p) {
+  if (!h) return MPGPU_ERR_DOMAIN;
+  if (!p) return MPGPU_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  cudaSetDevice(h->device);
+  CUDA_TRY(h, cudaIpcCloseMemHandle(p));
+  return MPGPU_OK;
+}
+
 // ---- accuracy metrics (metrics.cu) -------------------------------------------
 namespace {
 // elementwise metric kernel + reduction, then the three result records -> host SoA

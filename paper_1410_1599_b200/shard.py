@@ -276,6 +276,102 @@ class _FastRowOwned:
         return s
 
 
+class _FastRowOwnedP2P:
+    """Strassen / Winograd over N GPUs, one process each, with the exchange FUSED into the
+    producing kernels: every rank allocates its unit-product buffer (all units, its own unit
+    rows) with cudaMalloc and shares its CUDA IPC handle; each rank maps the others' buffers
+    (peer access over NVLink / NVSwitch) and hands mpgpu_fast_leaves_rows a device table of row
+    destinations, so the leaf GEMM's (or last local post-addition's) epilogue stores every
+    product row straight into the buffer of the rank that owns it.  No all-to-all, no packing,
+    no staging: the transfer overlaps the leaf math tile by tile.  Then mpgpu_fast_combine_rows
+    for the rank's rows, as _FastRowOwned.  Host barriers order the steps (products landed ->
+    combine; combine read -> next step's stores).  Precisions <= 1024 bits."""
+    replicated = False
+
+    def __init__(self, algo, n_min, da, db, dc, rank, world, group=None):
+        import torch
+        import torch.distributed as dist
+        from .mpmm import record_words
+        self.algo, self.n_min, self.da, self.db, self.dc = int(algo), n_min, da, db, dc
+        self.group, self.rank, self.world = group, rank, world
+        m, l, n = da.rows(), da.cols(), db.cols()
+        self.l = l
+        depth, leaves, *_ = fast_plan(m, l, n, n_min)
+        if depth == 0:
+            raise ValueError("leaf sharding needs a recursion (depth >= 1)")
+        self.up = choose_split(depth, world)
+        units = 7 ** (depth - self.up)
+        self.units = even_ranges(units, world)
+        self.shard = self.units[rank]
+        um, un = node_dims(m, l, n, n_min, depth - self.up)
+        self.rows = even_ranges(um, world)
+        self.my_rows = self.rows[rank]
+        rw = record_words(dc.m.nlimbs)
+        row_w, unit_w = un * rw, um * un * rw
+        h = dc._h
+        buf = C.c_void_p()
+        _raise_rc(h, _L.lib.mpgpu_malloc(h, C.c_size_t(4 * max(1, units * unit_w)), C.byref(buf)))
+        self.full_ptr = buf.value
+        hb = (C.c_uint8 * 64)()
+        _raise_rc(h, _L.lib.mpgpu_ipc_handle(h, C.c_void_p(self.full_ptr), hb))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(hb), group=group)
+        self.peers = []
+        base = []
+        for r_, hnd in enumerate(handles):
+            if r_ == rank:
+                base.append(self.full_ptr)
+                continue
+            p = C.c_void_p()
+            src = (C.c_uint8 * 64).from_buffer_copy(hnd)
+            _raise_rc(h, _L.lib.mpgpu_ipc_open(h, src, C.byref(p)))
+            self.peers.append(p.value)
+            base.append(p.value)
+        tab = [0] * um
+        for r_, rr in enumerate(self.rows):
+            for row in range(rr.lo, rr.hi):
+                tab[row] = base[r_] + 4 * ((self.shard.lo * um + row) * row_w)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.rowtab = torch.tensor(tab, dtype=torch.int64, device=dev)
+        self.c_rows = owned_c_rows(m, depth, depth - self.up, self.my_rows.lo, self.my_rows.hi)
+        self.mode = (f"row-owned p2p(up={self.up}, units={units}, per_rank={self.shard.per}, "
+                     f"unit_rows_per_rank={self.rows[0].per}; exchange fused into the leaf epilogue)")
+
+    def __call__(self):
+        import torch
+        import torch.distributed as dist
+        from .mpmm import Stats, _raise
+        st = _L.MpgpuStats()
+        h = self.dc._h
+        dist.barrier(group=self.group)  # every rank finished reading its buffer (previous step)
+        if self.shard.hi > self.shard.lo:
+            _raise(h, _L.lib.mpgpu_fast_leaves_rows(h, self.algo, self.n_min, C.byref(self.da.m), C.byref(self.db.m),
+                                                    self.up, self.shard.lo, self.shard.hi,
+                                                    C.c_void_p(self.rowtab.data_ptr()), C.byref(st)))
+        _L.lib.mpgpu_synchronize(h)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # every rank's product rows have landed
+        torch.cuda.synchronize()
+        st2 = _L.MpgpuStats()
+        _raise(h, _L.lib.mpgpu_fast_combine_rows(h, self.algo, self.n_min, self.l, self.up,
+                                                 C.c_void_p(self.full_ptr), self.my_rows.lo, self.my_rows.hi,
+                                                 C.byref(self.dc.m), C.byref(st2)))
+        s = Stats.of(st)
+        s.postadd_ms += st2.postadd_ms
+        s.launches += st2.launches
+        s.mul, s.addsub = _count(self.algo, self.da, self.db, self.n_min)
+        return s
+
+    def close(self):
+        h = self.dc._h
+        for p in self.peers:
+            _L.lib.mpgpu_ipc_close(h, C.c_void_p(p))
+        self.peers = []
+        if self.full_ptr:
+            _L.lib.mpgpu_free(h, C.c_void_p(self.full_ptr))
+            self.full_ptr = None
+
+
 def _staged(group) -> bool:
     """gloo cannot move CUDA tensors: stage the exchange through host memory (the CPU test of
     the real runners: 2 processes sharing one GPU, gloo over 127.0.0.1)."""
@@ -373,10 +469,11 @@ def _cuda_copy(h, dst: int, src: int, nbytes: int):
 
 
 def make_runner(algo, param, da, db, dc, rank: int, world: int, mode: str = "auto", group=None):
-    """mode: 'auto' (fast algorithms: leaf shards with the row-owned all-to-all combine;
-    simple/block: row shards), 'gather' (fast algorithms: leaf shards, all-gather of the
-    unit products and a replicated combine -- C complete on every rank), 'replicas'
-    (independent copies, weak scaling)."""
+    """mode: 'auto' (fast algorithms: leaf shards whose leaf epilogue stores the product rows
+    into their owners' buffers over peer memory (CUDA IPC), then the row-owned combine;
+    simple/block: row shards), 'a2a' (the same split with an NCCL all-to-all of the row slices
+    instead of the fused stores), 'gather' (leaf shards, all-gather of the unit products and a
+    replicated combine -- C complete on every rank), 'replicas' (independent copies, weak)."""
     from .mpmm import Algorithm
     if world <= 1 or mode == "replicas":
         return _Replica(algo, param, da, db, dc)
@@ -385,6 +482,8 @@ def make_runner(algo, param, da, db, dc, rank: int, world: int, mode: str = "aut
         if depth >= 1:
             if mode == "gather":
                 return _FastSharded(algo, param, da, db, dc, rank, world, group)
-            return _FastRowOwned(algo, param, da, db, dc, rank, world, group)
+            if mode == "a2a" or dc.m.nlimbs > 32:
+                return _FastRowOwned(algo, param, da, db, dc, rank, world, group)
+            return _FastRowOwnedP2P(algo, param, da, db, dc, rank, world, group)
         return _Replica(algo, param, da, db, dc)
     return _RowSharded(algo, param, da, db, dc, rank, world, group)

@@ -23,6 +23,8 @@ def main():
     out = []
     for algo, param, mode, (m, l, n), bits in [("winograd", 8, "auto", (96, 80, 72), 256),
                                                 ("strassen", 5, "auto", (45, 37, 51), 512),
+                                                ("winograd", 8, "a2a", (96, 80, 72), 256),
+                                                ("strassen", 6, "a2a", (61, 50, 47), 1024),
                                                 ("winograd", 8, "gather", (64, 64, 64), 128),
                                                 ("block", 16, "auto", (70, 48, 33), 256),
                                                 ("simple", 0, "auto", (33, 20, 17), 1024)]:
@@ -45,6 +47,9 @@ def main():
         cnt = P.count_fast(P.Algorithm[algo], m, l, n, max(1, param))
         out.append({"algo": algo, "mode": mode, "runner": runner.__class__.__name__, "rows": len(own), "m": m, "bad": bad,
                     "ops_ok": (st.mul, st.addsub) == (cnt.mul, cnt.addsub)})
+        if hasattr(runner, "close"):
+            dist.barrier()  # every peer is done with the shared buffers
+            runner.close()
         for x in (da, db, dc, ref):
             x.free()
     dist.destroy_process_group()

@@ -41,5 +41,5 @@ def test_runners_across_processes_bit_exact(world):
     for i in range(ncase):
         cases = [r["cases"][i] for r in results]
         assert all(c["bad"] == 0 and c["ops_ok"] for c in cases), cases
-        if cases[0]["runner"] == "_FastRowOwned":
+        if cases[0]["runner"] in ("_FastRowOwned", "_FastRowOwnedP2P"):
             assert sum(c["rows"] for c in cases) == cases[0]["m"]  # the owned rows partition C

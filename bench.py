@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--no-lu", action="store_true", help="skip the config-5 LU leg")
     ap.add_argument("--probe-world", action="store_true",
                     help="print this rank's (rank, world) as JSON and exit before touching CUDA (launcher test)")
-    ap.add_argument("--cfg4", action="store_true", help="also time config 4 (n=4096 @1024) at N=1")
-    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 leg at N>1")
+    ap.add_argument("--cfg4", action="store_true", help="(default) time config 4 (n=4096 @1024)")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-1 / config-3 legs")
     ap.add_argument("--shard", choices=["auto", "a2a", "gather", "replicas"], default="auto",
                     help="N>1: auto = leaf shards whose leaf epilogue stores the product rows into their owners' "
                          "buffers over peer memory (CUDA IPC, NVLink), then a row-owned combine (Strassen/Winograd), "
@@ -296,8 +297,11 @@ def main():
     if world > 1 and not args.no_e2e:
         e2e_res = e2e_dist(args, P, torch, dist, a, b, da, db, dc, runner, rank, world)
     big = None
-    if world > 1 and not args.no_cfg4 or args.cfg4:
+    if not args.no_cfg4:
         big = cfg4_leg(args, P, torch, dist, stream, flush, local, rank, world)
+    others = None
+    if world == 1 and not args.no_configs:
+        others = other_configs(args, P, torch, stream, flush, local)
 
     if rank != 0:
         if dist:
@@ -346,6 +350,8 @@ def main():
         line["e2e"] = e2e_res
     if big is not None:
         line["cfg4"] = big
+    if others is not None:
+        line["configs_1_3"] = others
     if not args.no_precision_sweep and world == 1:
         line["leaf_roofline_by_bits"] = precision_sweep(args, P, torch, IMAD_PER_CLK_PER_SM * sms * sm_max * 1e6 / 1e12)
     if not args.no_lu and world == 1:
@@ -459,13 +465,73 @@ def cfg4_leg(args, P, torch, dist, stream, flush, local, rank, world):
         return runner() if runner is not None else P.gemm_into(algo, nmin, da, db, dc)
 
     total_ms, leaf_ms, launches, st, clocks = timed_steps(args, torch, dist, stream, flush, step, local, 1, 1)
+    L = P.nlimbs_for(1024)
+    out = {"workload": "BASELINE config 4: MP GEMM n=4096 @1024-bit, winograd n_min=512 (depth 3)",
+           "value": n ** 3 / (total_ms * 1e-3), "unit": "madd/s", "ms_per_step": total_ms, "steps": 1, "warmup": 1,
+           "leaf_ms_rank0": float(np.mean(leaf_ms)), "leaf_madds_rank0": st.leaf_madds,
+           "imad_eq_per_madd": 2 * L * L, "runner": getattr(runner, "mode", "single GPU"), "clocks": clocks}
+    if world == 1:
+        # the same product at the cutoff chosen from the measured leaf throughput (deeper recursion,
+        # top levels depth-first beyond the scratch budget) -- an extension, reported beside
+        nm, depth, model_ms = P.choose_n_min(algo, 1024, n, n, n)
+        P.gemm_into(algo, P.AUTO_NMIN, da, db, dc)
+        sa = P.gemm_into(algo, P.AUTO_NMIN, da, db, dc)
+        out["auto_n_min"] = {"n_min": nm, "depth": depth, "model_ms": model_ms, "device_ms": sa.device_ms,
+                             "leaf_ms": sa.leaf_ms, "value": n ** 3 / (sa.device_ms * 1e-3)}
+        ref = ROOT / "profiles" / "r02_ref_cfg4_extrapolated.json"
+        if ref.exists():
+            try:
+                out["cpu_reference_extrapolated"] = json.loads(ref.read_text())
+            except Exception:
+                pass
+    if hasattr(runner, "close"):
+        if dist:
+            dist.barrier()
+        runner.close()
     for x in (da, db, dc):
         x.free()
-    L = P.nlimbs_for(1024)
-    return {"workload": "BASELINE config 4: MP GEMM n=4096 @1024-bit, winograd n_min=512 (depth 3)",
-            "value": n ** 3 / (total_ms * 1e-3), "unit": "madd/s", "ms_per_step": total_ms, "steps": 1, "warmup": 1,
-            "leaf_ms_rank0": float(np.mean(leaf_ms)), "leaf_madds_rank0": st.leaf_madds,
-            "imad_eq_per_madd": 2 * L * L, "runner": getattr(runner, "mode", "single GPU"), "clocks": clocks}
+    return out
+
+
+def other_configs(args, P, torch, stream, flush, local):
+    """BASELINE configs 1 and 3 on the same GPU (CUDA events, min of 5 after 2 warm-ups): cfg1 128^3
+    @128 bits -- Simple, Block 32, Strassen / Winograd cutoff 32 -- and cfg3 1001 x 777 x 1537 @512
+    bits, config-3 inputs, Winograd with pad-only odd handling at cutoffs 32 and 64.  Bit-exact
+    parity of these shapes is pinned by the test suite (tests/test_gpu_fullsize_hash.py holds the
+    compiled reference's SHA-256 of both cfg3 products); here each product is also checked against
+    the GPU Block product of the same operands (normwise bound for the fast algorithms)."""
+    import math
+    out = {}
+    cases = [("cfg1", 128, 128, 128, 128, P.gen_uniform_full, [("simple", 0), ("block", 32), ("strassen", 32),
+                                                               ("winograd", 32)]),
+             ("cfg3", 1001, 777, 1537, 512, P.gen_scaled, [("winograd", 32), ("winograd", 64)])]
+    for name, m, l, n, bits, gen, algos in cases:
+        ctx = P.PrecisionContext(bits)
+        a, b = gen(m, l, 1, ctx), gen(l, n, 2, ctx)
+        da, db = a.to_device(), b.to_device()
+        dc, ref = P.DeviceMatrix(m, n, ctx), P.DeviceMatrix(m, n, ctx)
+        P.gemm_into(P.Algorithm.block, 32, da, db, ref)
+        refh = ref.download()
+        res = []
+        for alg, param in algos:
+            algo = P.Algorithm[alg]
+            for _ in range(2):
+                P.gemm_into(algo, param, da, db, dc)
+            best = min((P.gemm_into(algo, param, da, db, dc) for _ in range(5)), key=lambda x: x.device_ms)
+            got = dc.download()
+            if alg == "block":
+                ok, err = P.identical(got, refh), None
+            else:
+                err = normwise_log2(P, got, refh, a, b)
+                ok = err <= math.log2(4.0) + math.log2(7) * math.log2(max(m, l, n)) - bits
+            res.append({"algorithm": alg, "n_min": param, "device_ms": best.device_ms, "leaf_ms": best.leaf_ms,
+                        "madd_per_s": m * l * n / (best.device_ms * 1e-3), "depth": best.depth,
+                        "check": "bit-identical to Block" if alg == "block" else
+                        {"log2_normwise_vs_block": err, "ok": bool(ok)}})
+        out[name] = {"shape": [m, l, n], "bits": bits, "runs": res}
+        for x in (da, db, dc, ref):
+            x.free()
+    return out
 
 
 def lu_leg(args, P, torch, stream, flush, leaf_peak_tiops):

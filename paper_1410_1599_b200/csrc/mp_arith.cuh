@@ -25,9 +25,6 @@
 #else
 #define MPG_UNROLL _Pragma("unroll")
 #endif
-#ifndef MPG_BRANCHFREE_CARRY
-#define MPG_BRANCHFREE_CARRY 0  // A/B: rounding carry-out fixups without branches
-#endif
 #ifndef MPG_ADD_IMAD_XOR_MAXL
 #define MPG_ADD_IMAD_XOR_MAXL 8  // measured: -1.2 % leaf time at 256 bits, +0.8 % at 512
 #endif
@@ -222,20 +219,12 @@ MPG_UNROLL
     }
     return;
   }
-#if MPG_BRANCHFREE_CARRY
-  {  // up_word only adds below the top bit: a carry-out leaves all limbs 0 -> 1000...0
-    const uint32_t c = add_word<L>(m, up_word);
-    m[L - 1] |= c << 31;
-    e += (int32_t)c;
-  }
-#else
   if (add_word<L>(m, up_word)) {
 MPG_UNROLL
     for (int k = 0; k < L - 1; ++k) m[k] = 0;
     m[L - 1] = 0x80000000u;
     e += 1;
   }
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -265,20 +254,12 @@ MPG_UNROLL
 MPG_UNROLL
       for (int k = 0; k < L; ++k) z.m[k] = __funnelshift_l(P[L + k - 1], P[L + k], t1);
       int32_t e = xe + y.e - (int32_t)t1;
-#if MPG_BRANCHFREE_CARRY
-      {  // carry out of an all-ones mantissa: the limbs wrapped to 0 -> 1000...0, exponent + 1
-        const uint32_t c = add_word<L>(z.m, up ? 1u : 0u);
-        z.m[L - 1] |= c << 31;
-        e += (int32_t)c;
-      }
-#else
       if (add_word<L>(z.m, up ? 1u : 0u)) {
 MPG_UNROLL
         for (int k = 0; k < L - 1; ++k) z.m[k] = 0;
         z.m[L - 1] = 0x80000000u;
         e += 1;
       }
-#endif
       z.e = e;
       return;
     }

@@ -221,3 +221,31 @@ def test_ragged_leaf_half_width_tiles(P, O, alg, param, bits):
         c = P.fast_mul(a, b, P.FastMMConfig(P.Algorithm.winograd, param), ctx).c
     want, _ = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
     assert P.identical(c, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg,param", [("simple", 0), ("block", 5), ("strassen", 3), ("winograd", 3)])
+@pytest.mark.parametrize("bits", [64, 256])
+def test_zeros_signed_zeros_and_exact_cancellation(P, O, alg, param, bits):
+    # sparse operands with +0 / -0 entries and rows that cancel exactly: the zero paths of the
+    # primitives (RN(-0 + -0) = -0, RN(x - x) = +0) inside the leaf, the pre- and post-additions
+    ctx = P.PrecisionContext(bits)
+    rng = np.random.default_rng(bits + param)
+    m, l, n = 23, 18, 21
+    a = P.gen_uniform_full(m, l, 5, ctx)
+    b = P.gen_uniform_full(l, n, 6, ctx)
+    za = rng.random(m * l) < 0.4
+    zb = rng.random(l * n) < 0.4
+    for x, z in ((a, za), (b, zb)):
+        x.limbs[:, z] = 0
+        x.exp[z] = P.EXP_ZERO
+        x.sign[z] = rng.integers(0, 2, int(z.sum())).astype(np.uint8)  # both zero signs
+    # row 1 of A = -(row 0): exact cancellation in every product row pair of the Winograd sums
+    a.limbs[:, l:2 * l] = a.limbs[:, 0:l]
+    a.exp[l:2 * l] = a.exp[0:l]
+    a.sign[l:2 * l] = 1 - a.sign[0:l]
+    ops = P.OpCounter()
+    c = _run(P, alg, param, a, b, ctx, ops)
+    want, wops = O.gemm(alg, param, O.OMat.of(a), O.OMat.of(b))
+    assert P.identical(c, want)  # signs of zeros included
+    assert (ops.mul, ops.addsub) == wops

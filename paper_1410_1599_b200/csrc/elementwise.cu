@@ -18,6 +18,10 @@
 #include "wkern.cuh"
 #endif
 
+#ifndef MPG_ADDS_HOIST
+#define MPG_ADDS_HOIST 1  // pre/post-additions: operands loaded up front for L <= 8
+#endif
+
 namespace mpg {
 
 namespace {
@@ -130,9 +134,19 @@ __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ p
     const uint32_t* P = parent + node * (int64_t)rows * cols * S;
     uint32_t* out = children + (node * 7 * per + e) * S;
     const int64_t cs = per * S;  // stride between sibling children
-    // quadrant q (0: 11, 1: 12, 2: 21, 3: 22) of the virtually zero-padded parent
+    // quadrant q (0: 11, 1: 12, 2: 21, 3: 22) of the virtually zero-padded parent; for small
+    // records all four are loaded up front (four independent loads in flight per thread)
+    constexpr bool HOIST = MPG_ADDS_HOIST && L <= 8;
+    MP<L> Q[HOIST ? 4 : 1];
+    if constexpr (HOIST) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, Q[q]);
+    }
     auto ld = [&](int q, MP<L>& x) {
-      load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x);
+      if constexpr (HOIST)
+        x = Q[q];
+      else
+        load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x);
     };
     auto put = [&](int child, const MP<L>& x) { store_rec<L>(out + child * cs, x); };
     auto sum = [&](int qa, int qb, uint32_t neg, int child) {
@@ -269,15 +283,28 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
     const uint32_t* M = children + (node * 7 * per + e) * S;
     const int64_t cs = per * S;
     uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    // small records: all seven children loaded up front (independent loads in flight)
+    constexpr bool HOIST = MPG_ADDS_HOIST && L <= 8;
+    MP<L> Mv[HOIST ? 7 : 1];
+    if constexpr (HOIST) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) load_rec<L>(M + k * cs, Mv[k]);
+    }
+    auto ldc = [&](int k, MP<L>& x) {
+      if constexpr (HOIST)
+        x = Mv[k];
+      else
+        load_rec<L>(M + k * cs, x);
+    };
     if (algo == 3) {
       // T1 = M1+M2, T2 = T1+M4; C11 = M2+M3, C12 = (T1+M5)+M6, C21 = T2-M7, C22 = T2+M5
       MP<L> m1, m2, t1, t2, u, v;
-      load_rec<L>(M + 0 * cs, m1);
-      load_rec<L>(M + 1 * cs, m2);
+      ldc(0, m1);
+      ldc(1, m2);
       mp_add<L>(m1, m2, 0u, sh, t1);
       {
         MP<L> m4;
-        load_rec<L>(M + 3 * cs, m4);
+        ldc(3, m4);
         mp_add<L>(t1, m4, 0u, sh, t2);
       }
       if (t_out) {
@@ -286,22 +313,22 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
       }
       {
         MP<L> m3;
-        load_rec<L>(M + 2 * cs, m3);
+        ldc(2, m3);
         mp_add<L>(m2, m3, 0u, sh, u);
         store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
       }
       MP<L> m5;
-      load_rec<L>(M + 4 * cs, m5);
+      ldc(4, m5);
       {
         MP<L> m6;
-        load_rec<L>(M + 5 * cs, m6);
+        ldc(5, m6);
         mp_add<L>(t1, m5, 0u, sh, u);
         mp_add<L>(u, m6, 0u, sh, v);
         store_if<L>(P, rows, cols, r, c + hc, v, err, rowtab, node);
       }
       {
         MP<L> m7;
-        load_rec<L>(M + 6 * cs, m7);
+        ldc(6, m7);
         mp_add<L>(t2, m7, 1u, sh, u);
         store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
       }
@@ -310,30 +337,30 @@ __global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, 
     } else {
       // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
       MP<L> p1, p4, p5, u, v;
-      load_rec<L>(M + 0 * cs, p1);
-      load_rec<L>(M + 3 * cs, p4);
-      load_rec<L>(M + 4 * cs, p5);
+      ldc(0, p1);
+      ldc(3, p4);
+      ldc(4, p5);
       mp_add<L>(p1, p4, 0u, sh, u);
       mp_add<L>(u, p5, 1u, sh, v);
       {
         MP<L> p7;
-        load_rec<L>(M + 6 * cs, p7);
+        ldc(6, p7);
         mp_add<L>(v, p7, 0u, sh, u);
         store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
       }
       MP<L> p3;
-      load_rec<L>(M + 2 * cs, p3);
+      ldc(2, p3);
       mp_add<L>(p3, p5, 0u, sh, u);
       store_if<L>(P, rows, cols, r, c + hc, u, err, rowtab, node);
       MP<L> p2;
-      load_rec<L>(M + 1 * cs, p2);
+      ldc(1, p2);
       mp_add<L>(p2, p4, 0u, sh, u);
       store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
       mp_add<L>(p1, p3, 0u, sh, u);
       mp_add<L>(u, p2, 1u, sh, v);
       {
         MP<L> p6;
-        load_rec<L>(M + 5 * cs, p6);
+        ldc(5, p6);
         mp_add<L>(v, p6, 0u, sh, u);
         store_if<L>(P, rows, cols, r + hr, c + hc, u, err, rowtab, node);
       }

@@ -33,13 +33,16 @@ def main():
         A = gen(m, l, 1, ctx).to_device()
         B = gen(l, n, 2, ctx).to_device()
         C = P.DeviceMatrix(m, n, ctx)
-        leaf, dev = [], []
+        leaf, dev, pre, post = [], [], [], []
         for _ in range(a.reps + 1):
             st = P.gemm_into(algo, a.n_min if algo != P.Algorithm.simple else 0, A, B, C)
             leaf.append(st.leaf_ms)
             dev.append(st.device_ms)
+            pre.append(st.preadd_ms)
+            post.append(st.postadd_ms)
         print(json.dumps({"tag": a.tag, "algo": a.algo, "shape": [m, l, n], "n_min": a.n_min, "bits": bits,
-                          "leaf_ms": min(leaf[1:]), "device_ms": min(dev[1:])}), flush=True)
+                          "leaf_ms": min(leaf[1:]), "device_ms": min(dev[1:]), "preadd_ms": min(pre[1:]),
+                          "postadd_ms": min(post[1:])}), flush=True)
 
 
 if __name__ == "__main__":

@@ -104,10 +104,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
 #define MPG_KK_UNROLL_8 2  // measured: 2 beats 1 and 4 at 256 bits (and loses at L >= 16)
 #endif
 
-#ifndef MPG_PHASE
-#define MPG_PHASE 0
-#endif
-
 #ifndef MPG_TM_8
 #define MPG_TM_8 16
 #endif
@@ -244,18 +240,6 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 
   int next_b = g.kb;  // k at which the next Block k-tile starts
 
-  // MPG_PHASE: odd warps defer the accumulate of each k-tile's last product past the
-  // barrier, so after every barrier half the warps start in the FMA-heavy product phase
-  // and half in the ALU-heavy accumulate phase (same operation order per element)
-  const bool lag = MPG_PHASE && !FOLD && ((tid >> 5) & 1);
-  MP<L> tpend[U];
-  bool have_pend = false;
-  auto prod = [&](const uint32_t* ar, const uint32_t* bc, MP<L>& t) {
-    MP<L> b;
-    MPG_LOAD<L>(bc, b);
-    mp_mul_g<L>([&](int q) { return ar[q]; }, (int32_t)ar[L], ar[L + 1], b, g.sh, t);
-  };
-
   if (tid == 0) {
     mbar_init1(&s_bar[0]);
     mbar_init1(&s_bar[1]);
@@ -276,14 +260,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     if (active) {
       const uint32_t* a_rows = sA + (kt & 1) * A_WORDS + ty * TK * S;
       const uint32_t* b_cols = sB + (kt & 1) * B_WORDS + tx * S;
-      int kend = min(TK, g.l - kt * TK);
-      if (MPG_PHASE && lag) {
-        if (have_pend) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) mp_add<L>(pacc[u], tpend[u], 0u, g.sh, pacc[u]);
-        }
-        kend -= 1;
-      }
+      const int kend = min(TK, g.l - kt * TK);
 #pragma unroll GemmCfg<L>::KU
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
@@ -321,17 +298,8 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 #endif
         }
       }
-      if (MPG_PHASE && lag) {  // the tile's last product; its accumulate waits for the next tile
-#pragma unroll
-        for (int u = 0; u < U; ++u) prod(a_rows + kend * S, b_cols + (kend * TNB + u * TN) * S, tpend[u]);
-        have_pend = true;
-      }
     }
     __syncthreads();
-  }
-  if (MPG_PHASE && lag && have_pend) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) mp_add<L>(pacc[u], tpend[u], 0u, g.sh, pacc[u]);
   }
   if (!active) return;
 #pragma unroll

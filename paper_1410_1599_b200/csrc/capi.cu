@@ -35,6 +35,9 @@ struct mpgpu_handle {
   // LU look-ahead: the next panel runs on a high-priority stream beside the Schur update
   cudaStream_t hi = nullptr;
   cudaEvent_t ev_la = nullptr, ev_lp = nullptr;
+  // pipelined host GEMM: downloads on their own stream; per-quadrant events
+  cudaStream_t dl = nullptr;
+  cudaEvent_t pev[16] = {};
 };
 
 namespace {
@@ -639,7 +642,10 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
 template <int L>
 int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A, int64_t lda, const uint32_t* B,
                     int64_t ldb, int64_t m, int64_t l, int64_t n, int64_t ulo, int64_t uhi, int up_levels,
-                    uint32_t* out, int sh, mpgpu_stats* stats, const uint64_t* rowtab = nullptr) {
+                    uint32_t* out, int sh, mpgpu_stats* stats, const uint64_t* rowtab = nullptr,
+                    const uint32_t* l1A = nullptr, const uint32_t* l1B = nullptr) {
+  // l1A / l1B (optional): the 7 level-1 operands of each side already formed (dense, child
+  // slot c at c * m1 * l1 / l1 * n1 records) -- the level-0 pre-additions are skipped
   constexpr int S = rec_stride(L);
   cudaStream_t st = h->stream;
   const bool timing = stats != nullptr;
@@ -649,6 +655,7 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
   if (d == 0) return fail(h, MPGPU_ERR_DOMAIN, "fast_leaves: the product is a base case (depth 0)");
   if (up_levels < 0 || up_levels > d) return fail(h, MPGPU_ERR_DIMENSION, "fast_leaves: bad output level");
   const int ol = d - up_levels;  // level of the output nodes
+  if (l1A && ol < 1) return fail(h, MPGPU_ERR_DIMENSION, "fast_leaves: level-1 operands need units below the top");
   int64_t units = 1, span = 1;  // nodes at level ol; leaves per unit
   for (int i = 0; i < ol; ++i) units *= 7;
   for (int i = 0; i < up_levels; ++i) span *= 7;
@@ -666,12 +673,12 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
   DevBuf a0, b0;
   const uint32_t* pa = A;
   const uint32_t* pb = B;
-  if (lda != l) {
+  if (lda != l && !l1A) {
     CUDA_TRY(h, a0.alloc(h, sizeof(uint32_t) * S * m * l));
     mpg::launch_copy2d<L>(A, lda, a0.u32(), l, (int)m, (int)l, st);
     pa = a0.u32();
   }
-  if (ldb != n) {
+  if (ldb != n && !l1A) {
     CUDA_TRY(h, b0.alloc(h, sizeof(uint32_t) * S * l * n));
     mpg::launch_copy2d<L>(B, ldb, b0.u32(), n, (int)l, (int)n, st);
     pb = b0.u32();
@@ -681,13 +688,19 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
   std::vector<int64_t> bs(d + 1), bn(d + 1);
   bs[0] = 0;
   bn[0] = 1;
+  auto bufA = [&](int lev) -> const uint32_t* { return (lev == 1 && l1A) ? l1A : opA[lev].u32(); };
+  auto bufB = [&](int lev) -> const uint32_t* { return (lev == 1 && l1A) ? l1B : opB[lev].u32(); };
+  if (l1A) {
+    bs[1] = 0;
+    bn[1] = 7;
+  }
   Timer tpre(timing, st);
-  for (int lev = 0; lev < d; ++lev) {
+  for (int lev = l1A ? 1 : 0; lev < d; ++lev) {
     const Level& P = lv[lev];
     const Level& Q = lv[lev + 1];
     const int64_t p0 = s[lev], np = e[lev] - s[lev];
-    const uint32_t* srcA = lev == 0 ? pa : opA[lev].u32() + (p0 - bs[lev]) * P.m * P.l * S;
-    const uint32_t* srcB = lev == 0 ? pb : opB[lev].u32() + (p0 - bs[lev]) * P.l * P.n * S;
+    const uint32_t* srcA = lev == 0 ? pa : bufA(lev) + (p0 - bs[lev]) * P.m * P.l * S;
+    const uint32_t* srcB = lev == 0 ? pb : bufB(lev) + (p0 - bs[lev]) * P.l * P.n * S;
     bs[lev + 1] = 7 * p0;
     bn[lev + 1] = 7 * np;
     CUDA_TRY(h, opA[lev + 1].alloc(h, sizeof(uint32_t) * S * bn[lev + 1] * Q.m * Q.l));
@@ -705,8 +718,8 @@ int run_fast_leaves(mpgpu_handle* h, int algo, int64_t n_min, const uint32_t* A,
   {
     Timer tl(timing, st);
     mpg::GemmArgs g{};
-    g.A = opA[d].u32() + (lo - bs[d]) * D.m * D.l * S;
-    g.B = opB[d].u32() + (lo - bs[d]) * D.l * D.n * S;
+    g.A = bufA(d) + (lo - bs[d]) * D.m * D.l * S;
+    g.B = bufB(d) + (lo - bs[d]) * D.l * D.n * S;
     DevBuf leafbuf;
     if (up_levels == 0) {
       g.C = out;
@@ -1014,6 +1027,232 @@ int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint3
   return MPGPU_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined host GEMM (Winograd, even m, l, n): the operands travel to the device by
+// quadrant and the product back by output quadrant, so the PCIe transfers run under
+// the products instead of before and after them.  The top level of fast_mul_rec
+// (fastmm.hpp:174-198) is unrolled here:
+//   m2 = a11 b11 and m3 = a12 b21 need one quadrant of A and of B each: each starts as
+//   soon as its quadrants are on the device, as its own breadth-first recursion on the
+//   views (fast_mul_rec's rec(a11, b11), rec(a12, b21)); C11 = m2 + m3 then leaves at
+//   once.  m1, (m4, m5) and (m6, m7) follow as child ranges of the full recursion
+//   (run_fast_leaves: the top-level sums s1..s8, then their subtrees);
+//   C22 = (t1 + m4) + m5 with t1 = m1 + m2 leaves next, C12 = (t1 + m5) + m6 and
+//   C21 = (t1 + m4) - m7 last.  Every element sees the reference's operation sequence:
+//   bit-identical to mpgpu_gemm.
+// ---------------------------------------------------------------------------
+static bool host_pipe_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MPGPU_HOST_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// the pipeline pays for itself once the product is a few milliseconds
+static bool host_pipe_applies(int algo, int64_t n_min, int64_t m, int64_t l, int64_t n, int32_t Lh, int L) {
+  return host_pipe_enabled() && algo == MPGPU_WINOGRAD && Lh == L && L <= 32 && m % 2 == 0 && l % 2 == 0 && n % 2 == 0 &&
+         std::min({m, l, n}) > n_min && (double)m * l * n >= (double)(1 << 21);
+}
+
+template <int L>
+int gemm_host_pipe(mpgpu_handle* h, int64_t n_min, int32_t prec, int64_t m, int64_t l, int64_t n,
+                   const uint32_t* al, const int32_t* ae, const uint8_t* as, const uint32_t* bl, const int32_t* be,
+                   const uint8_t* bs, uint32_t* cl, int32_t* ce, uint8_t* cs, mpgpu_stats* stats) {
+  if constexpr (L > 32) {
+    return fail(h, MPGPU_ERR_DOMAIN, "internal: pipelined host GEMM is for L <= 32");
+  } else {
+  constexpr int S = rec_stride(L);
+  const int sh = 32 * L - prec;
+  const int64_t hm = m / 2, hl = l / 2, hn = n / 2;
+  const int64_t qa = hm * hl, qb = hl * hn, qc = hm * hn;
+  const size_t R = sizeof(uint32_t) * S;
+  const size_t soa = sizeof(uint32_t) * L + sizeof(int32_t) + 1;  // SoA bytes per element
+  auto al256 = [](size_t b) { return (b + 255) / 256 * 256; };    // every staging block 256-byte aligned
+  const int d = (int)plan_levels(m, l, n, n_min).size() - 1;
+  cudaStream_t st = h->stream;
+  if (!h->aux) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+    CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+  }
+  if (!h->dl) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->dl, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->pev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* up = h->pev;         // [0, 8): quadrant copies arrived
+  cudaEvent_t* cdone = h->pev + 8;  // [8, 12): output quadrant converted for the copy back
+  cudaEvent_t ready = h->pev[12], dl_done = h->pev[13];
+  Timer total(stats != nullptr, st);
+  DevBuf da, db, l1a, l1b, stage, mq, tq, cq, dstage;
+  CUDA_TRY(h, da.alloc(h, R * m * l));
+  CUDA_TRY(h, db.alloc(h, R * l * n));
+  CUDA_TRY(h, l1a.alloc(h, R * 7 * qa));  // level-1 operands, child slots (see slot below)
+  CUDA_TRY(h, l1b.alloc(h, R * 7 * qb));
+  CUDA_TRY(h, stage.alloc(h, 4 * al256(soa * (size_t)qa) + 4 * al256(soa * (size_t)qb)));
+  CUDA_TRY(h, mq.alloc(h, R * 7 * qc));  // level-1 products, by slot
+  CUDA_TRY(h, tq.alloc(h, R * 3 * qc));  // t1, t2, t1 + m5
+  CUDA_TRY(h, cq.alloc(h, R * 4 * qc));  // C11, C12, C21, C22
+  CUDA_TRY(h, dstage.alloc(h, 4 * al256(soa * (size_t)qc)));
+  CUDA_TRY(h, cudaMemsetAsync(h->d_err, 0, 4 * sizeof(uint32_t), st));
+  CUDA_TRY(h, cudaEventRecord(ready, st));  // the buffers exist before the other streams touch them
+  CUDA_TRY(h, cudaStreamWaitEvent(h->aux, ready, 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->dl, ready, 0));
+  // every exit from here: the handle's stream (which frees the buffers) first waits for the others
+  struct Join {
+    mpgpu_handle* h;
+    cudaEvent_t a, b;
+    ~Join() {
+      cudaEventRecord(a, h->aux);
+      cudaStreamWaitEvent(h->stream, a, 0);
+      cudaEventRecord(b, h->dl);
+      cudaStreamWaitEvent(h->stream, b, 0);
+    }
+  } join{h, h->ev_a, dl_done};
+  // MPGPU_PIPE_TRACE=1: per-phase event times to stderr (diagnostics)
+  static const bool trace = std::getenv("MPGPU_PIPE_TRACE") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  cudaEvent_t t0 = nullptr;
+  auto mark = [&](const char* what, cudaStream_t on) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, on);
+    marks.push_back({what, e});
+  };
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, st);
+  }
+
+  // ---- copies in (aux stream, copy engine only): SoA planes of one quadrant into staging
+  struct Quad {
+    int side, q;
+    uint32_t* pl;
+    int32_t* pe;
+    uint8_t* ps;
+  };
+  // order: what m2 = a11 b11, then m3 = a12 b21, then the rest need
+  Quad order[8] = {{0, 0}, {1, 0}, {0, 1}, {1, 2}, {0, 2}, {0, 3}, {1, 1}, {1, 3}};
+  uint8_t* sp = static_cast<uint8_t*>(stage.p);
+  for (int i = 0; i < 8; ++i) {
+    Quad& u = order[i];
+    const int64_t rows = u.side ? l : m, cols = u.side ? n : l, hr = rows / 2, hc = cols / 2, N = hr * hc;
+    const uint32_t* hl_ = u.side ? bl : al;
+    const int32_t* he = u.side ? be : ae;
+    const uint8_t* hs = u.side ? bs : as;
+    u.pl = reinterpret_cast<uint32_t*>(sp);
+    u.pe = reinterpret_cast<int32_t*>(u.pl + (size_t)L * N);
+    u.ps = reinterpret_cast<uint8_t*>(u.pe + N);
+    sp += al256(soa * (size_t)N);
+    const int64_t off = (u.q >> 1) * hr * cols + (u.q & 1) * hc;
+    const size_t hp = sizeof(uint32_t) * (size_t)cols;
+    for (int j = 0; j < L; ++j)
+      CUDA_TRY(h, cudaMemcpy2DAsync(u.pl + (size_t)j * N, sizeof(uint32_t) * hc, hl_ + (size_t)j * rows * cols + off,
+                                    hp, sizeof(uint32_t) * hc, hr, cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaMemcpy2DAsync(u.pe, sizeof(int32_t) * hc, he + off, sizeof(int32_t) * cols,
+                                  sizeof(int32_t) * hc, hr, cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaMemcpy2DAsync(u.ps, hc, hs + off, cols, hc, hr, cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaEventRecord(up[i], h->aux));
+    mark("copy in", h->aux);
+  }
+  // level-1 child c of fast_mul_rec lives in slot[c]: m2, m3 first (slots 0, 1), then
+  // m1, m4, m5 (2..4) and m6, m7 (5, 6) -- contiguous unit ranges for run_fast_leaves
+  constexpr int8_t slot[7] = {2, 0, 1, 3, 4, 5, 6};
+  // layout conversion of copy i on the handle's stream, into the full operand and, for the
+  // quadrants that are level-1 operands as they are (a11, b11, a12, b21), into their slot
+  auto convert = [&](int i, int l1slot) -> int {
+    const Quad& u = order[i];
+    const int64_t rows = u.side ? l : m, cols = u.side ? n : l, hr = rows / 2, hc = cols / 2, N = hr * hc;
+    CUDA_TRY(h, cudaStreamWaitEvent(st, up[i], 0));
+    uint32_t* full = u.side ? db.u32() : da.u32();
+    const int64_t off = (u.q >> 1) * hr * cols + (u.q & 1) * hc;
+    mpg::launch_soa2rec_2d<L>(u.pl, u.pe, u.ps, hr, hc, N, full + off * S, cols, st);
+    if (l1slot >= 0)
+      mpg::launch_soa2rec<L>(u.pl, u.pe, u.ps, N, N, (u.side ? l1b.u32() : l1a.u32()) + (size_t)l1slot * N * S, st);
+    return MPGPU_OK;
+  };
+
+  // ---- copies out (dl stream): output quadrant q, converted on the handle's stream
+  uint8_t* dp = static_cast<uint8_t*>(dstage.p);
+  auto Cq = [&](int q) { return cq.u32() + (size_t)q * qc * S; };
+  auto download_quad = [&](int q) -> int {
+    uint32_t* pl = reinterpret_cast<uint32_t*>(dp + q * al256(soa * (size_t)qc));
+    int32_t* pe = reinterpret_cast<int32_t*>(pl + (size_t)L * qc);
+    uint8_t* ps = reinterpret_cast<uint8_t*>(pe + qc);
+    mpg::launch_rec2soa<L>(Cq(q), qc, pl, pe, ps, qc, st);
+    CUDA_TRY(h, cudaEventRecord(cdone[q], st));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->dl, cdone[q], 0));
+    const int64_t off = (q >> 1) * hm * n + (q & 1) * hn;
+    const size_t hp = sizeof(uint32_t) * (size_t)n;
+    for (int j = 0; j < L; ++j)
+      CUDA_TRY(h, cudaMemcpy2DAsync(cl + (size_t)j * m * n + off, hp, pl + (size_t)j * qc, sizeof(uint32_t) * hn,
+                                    sizeof(uint32_t) * hn, hm, cudaMemcpyDeviceToHost, h->dl));
+    CUDA_TRY(h, cudaMemcpy2DAsync(ce + off, sizeof(int32_t) * n, pe, sizeof(int32_t) * hn, sizeof(int32_t) * hn, hm,
+                                  cudaMemcpyDeviceToHost, h->dl));
+    CUDA_TRY(h, cudaMemcpy2DAsync(cs + off, n, ps, hn, hn, hm, cudaMemcpyDeviceToHost, h->dl));
+    mark("copy out", h->dl);
+    return MPGPU_OK;
+  };
+
+  // ---- products and the top-level post-additions (handle's stream)
+  auto Ms = [&](int child) { return mq.u32() + (size_t)slot[child] * qc * S; };  // m_{child+1}
+  uint32_t* t1 = tq.u32();
+  uint32_t* t2 = t1 + (size_t)qc * S;
+  uint32_t* u5 = t2 + (size_t)qc * S;
+  auto add = [&](const uint32_t* x, const uint32_t* y, uint32_t* z, int is_sub) {
+    mpg::launch_addsub<L>(x, y, z, qc, is_sub, sh, h->d_err, st);
+  };
+  auto products = [&](int slot_lo, int slot_hi) {  // level-1 products of slots [lo, hi)
+    return run_fast_leaves<L>(h, MPGPU_WINOGRAD, n_min, da.u32(), l, db.u32(), n, m, l, n, slot_lo, slot_hi, d - 1,
+                              mq.u32() + (size_t)slot_lo * qc * S, sh, nullptr, nullptr, l1a.u32(), l1b.u32());
+  };
+  int rc;
+  if ((rc = convert(0, 0)) || (rc = convert(1, 0)) || (rc = products(0, 1))) return rc;  // m2 = a11 b11
+  mark("m2", st);
+  if ((rc = convert(2, 1)) || (rc = convert(3, 1)) || (rc = products(1, 2))) return rc;  // m3 = a12 b21
+  add(Ms(1), Ms(2), Cq(0), 0);                                                           // C11 = m2 + m3
+  mark("m3 C11", st);
+  if ((rc = download_quad(0))) return rc;
+  for (int i = 4; i < 8; ++i)
+    if ((rc = convert(i, -1))) return rc;
+  const mpg::ChildSlots rest{{slot[0], -1, -1, slot[3], slot[4], slot[5], slot[6]}};
+  mpg::launch_preadd_slots<L>(MPGPU_WINOGRAD, 0, da.u32(), (int)m, (int)l, l1a.u32(), rest, sh, st);  // s1..s4
+  mpg::launch_preadd_slots<L>(MPGPU_WINOGRAD, 1, db.u32(), (int)l, (int)n, l1b.u32(), rest, sh, st);  // s5..s8
+  if ((rc = products(2, 5))) return rc;  // m1 = s2 s6, m4 = s3 s7, m5 = s1 s5
+  add(Ms(0), Ms(1), t1, 0);              // t1 = m1 + m2
+  add(t1, Ms(3), t2, 0);                 // t2 = t1 + m4
+  add(t2, Ms(4), Cq(3), 0);              // C22 = t2 + m5
+  mark("m1 m4 m5 C22", st);
+  if ((rc = download_quad(3))) return rc;
+  // m6 and m7 apart: C12 goes back while m7 is computed
+  if ((rc = products(5, 6))) return rc;  // m6 = s4 b22
+  add(t1, Ms(4), u5, 0);                 // t1 + m5
+  add(u5, Ms(5), Cq(1), 0);              // C12 = (t1 + m5) + m6
+  mark("m6 C12", st);
+  if ((rc = download_quad(1))) return rc;
+  if ((rc = products(6, 7))) return rc;  // m7 = a22 s8
+  add(t2, Ms(6), Cq(2), 1);              // C21 = t2 - m7
+  mark("m7 C21", st);
+  if ((rc = download_quad(2))) return rc;
+  if (trace) {
+    cudaDeviceSynchronize();
+    for (auto& mk : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t0, mk.second);
+      fprintf(stderr, "[pipe] %-16s %8.3f ms\n", mk.first, ms);
+      cudaEventDestroy(mk.second);
+    }
+    cudaEventDestroy(t0);
+  }
+  if (stats) {
+    total.stop(&stats->device_ms);
+    stats->depth = d;
+  }
+  return MPGPU_OK;
+  }
+}
+
 // ===========================================================================
 extern "C" {
 
@@ -1060,6 +1299,12 @@ void mpgpu_destroy(mpgpu_handle* h) {
   }
   if (h->ev_la) cudaEventDestroy(h->ev_la);
   if (h->ev_lp) cudaEventDestroy(h->ev_lp);
+  if (h->dl) {
+    cudaStreamSynchronize(h->dl);
+    cudaStreamDestroy(h->dl);
+  }
+  for (cudaEvent_t e : h->pev)
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 
@@ -1291,6 +1536,22 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(h->mu);
   cudaSetDevice(h->device);
+  if (host_pipe_applies(algo, param, m, l, n, Lh, L)) {
+    if (stats) {
+      std::memset(stats, 0, sizeof *stats);
+      uint64_t c[2];
+      count_fast_rec(algo, m, l, n, param, c);
+      stats->mul = c[0];
+      stats->addsub = c[1];
+    }
+    rc = dispatch_L(L, [&](auto Lc) {
+      return gemm_host_pipe<decltype(Lc)::value>(h, param, prec, m, l, n, al, ae, as, bl, be, bs, cl, ce, cs, stats);
+    });
+    if (rc) return rc;
+    rc = check_err(h);
+    flush_timers();
+    return rc;
+  }
   const size_t S4 = sizeof(uint32_t) * rec_stride(L);
   DevBuf da, db, dc, sa, sb, sc;
   CUDA_TRY(h, da.alloc(h, S4 * m * l));

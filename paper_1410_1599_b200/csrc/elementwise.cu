@@ -48,6 +48,26 @@ __global__ void soa2rec_kernel(const uint32_t* __restrict__ limbs, const int32_t
   }
 }
 
+// SoA planes of a dense rows x cols block -> records of a strided matrix (leading
+// dimension ldr): one quadrant of the pipelined host GEMM's operands
+template <int L>
+__global__ void soa2rec2d_kernel(const uint32_t* __restrict__ limbs, const int32_t* __restrict__ exp,
+                                 const uint8_t* __restrict__ sign, int64_t rows, int64_t cols, int64_t ps,
+                                 uint32_t* __restrict__ rec, int64_t ldr) {
+  constexpr int S = rec_stride(L);
+  const int64_t N = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    MP<L> x;
+#pragma unroll
+    for (int k = 0; k < L; ++k) x.m[k] = limbs[k * ps + e];
+    x.e = exp[e];
+    x.s = sign[e];
+    store_rec<L>(rec + (r * ldr + c) * S, x);
+  }
+}
+
 template <int L>
 __global__ void rec2soa_kernel(const uint32_t* __restrict__ rec, int64_t N, uint32_t* __restrict__ limbs,
                                int32_t* __restrict__ exp, uint8_t* __restrict__ sign, int64_t ps) {
@@ -121,7 +141,7 @@ __device__ __forceinline__ void load_padded(const uint32_t* P, int rows, int col
 // 1024-bit instantiation stays in registers.
 template <int L>
 __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
-                              int rows, int cols, uint32_t* __restrict__ children, int sh) {
+                              int rows, int cols, uint32_t* __restrict__ children, int sh, ChildSlots slots) {
   constexpr int S = rec_stride(L);
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
   const int64_t per = (int64_t)hr * hc;
@@ -148,7 +168,11 @@ __global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ p
       else
         load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x);
     };
-    auto put = [&](int child, const MP<L>& x) { store_rec<L>(out + child * cs, x); };
+    // slots.s[child]: output slot of each child, < 0: not produced (the pipelined host GEMM
+    // forms its top-level children in two steps); the identity map otherwise
+    auto put = [&](int child, const MP<L>& x) {
+      if (slots.s[child] >= 0) store_rec<L>(out + slots.s[child] * cs, x);
+    };
     auto sum = [&](int qa, int qb, uint32_t neg, int child) {
       MP<L> x, y;
       ld(qa, x);
@@ -415,6 +439,12 @@ void launch_soa2rec(const uint32_t* limbs, const int32_t* exp, const uint8_t* si
   soa2rec_kernel<L><<<grid_for(N), NT, 0, st>>>(limbs, exp, sign, N, ps, rec);
 }
 template <int L>
+void launch_soa2rec_2d(const uint32_t* limbs, const int32_t* exp, const uint8_t* sign, int64_t rows, int64_t cols,
+                       int64_t ps, uint32_t* rec, int64_t ldr, cudaStream_t st) {
+  if (rows * cols <= 0) return;
+  soa2rec2d_kernel<L><<<grid_for(rows * cols), NT, 0, st>>>(limbs, exp, sign, rows, cols, ps, rec, ldr);
+}
+template <int L>
 void launch_rec2soa(const uint32_t* rec, int64_t N, uint32_t* limbs, int32_t* exp, uint8_t* sign,
                     int64_t ps, cudaStream_t st) {
   rec2soa_kernel<L><<<grid_for(N), NT, 0, st>>>(rec, N, limbs, exp, sign, ps);
@@ -446,7 +476,14 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
     if (wmp::enabled()) return wmp::launch_preadd<L / 32>(algo, side, parent, nodes, rows, cols, children, sh, st);
 #endif
   const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
-  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh);
+  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh,
+                                                    ChildSlots{{0, 1, 2, 3, 4, 5, 6}});
+}
+template <int L>
+void launch_preadd_slots(int algo, int side, const uint32_t* parent, int rows, int cols, uint32_t* children,
+                         ChildSlots slots, int sh, cudaStream_t st) {
+  const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2);
+  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, 1, rows, cols, children, sh, slots);
 }
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
@@ -484,6 +521,8 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
                                   uint32_t*, cudaStream_t);                                             \
   template void launch_rec2soa<L>(const uint32_t*, int64_t, uint32_t*, int32_t*, uint8_t*, int64_t,    \
                                   cudaStream_t);                                                        \
+  template void launch_soa2rec_2d<L>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t, \
+                                     int64_t, uint32_t*, int64_t, cudaStream_t);                        \
   template void launch_addsub<L>(const uint32_t*, const uint32_t*, uint32_t*, int64_t, int, int,        \
                                  uint32_t*, cudaStream_t);                                              \
   template void launch_vec_op<L>(int, const uint32_t*, const uint32_t*, uint32_t*, int64_t, int,        \
@@ -512,6 +551,15 @@ MPG_INST(4)
 MPG_INST(8)
 MPG_INST(16)
 MPG_INST(32)
+#define MPG_INST_SLOTS(L)                                                                                     \
+  template void launch_preadd_slots<L>(int, int, const uint32_t*, int, int, uint32_t*, ChildSlots, int, \
+                                       cudaStream_t);
+MPG_INST_SLOTS(1)
+MPG_INST_SLOTS(2)
+MPG_INST_SLOTS(4)
+MPG_INST_SLOTS(8)
+MPG_INST_SLOTS(16)
+MPG_INST_SLOTS(32)
 #endif
 
 }  // namespace mpg

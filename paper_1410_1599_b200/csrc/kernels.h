@@ -61,11 +61,20 @@ void launch_soa2rec(const uint32_t* limbs, const int32_t* exp, const uint8_t* si
 template <int L>
 void launch_rec2soa(const uint32_t* rec, int64_t N, uint32_t* limbs, int32_t* exp, uint8_t* sign,
                     int64_t plane_stride, cudaStream_t st);
+// a dense rows x cols block of SoA planes into a strided record matrix (leading dim ldr)
+template <int L>
+void launch_soa2rec_2d(const uint32_t* limbs, const int32_t* exp, const uint8_t* sign, int64_t rows, int64_t cols,
+                       int64_t plane_stride, uint32_t* rec, int64_t ldr, cudaStream_t st);
 
 // elementwise C = A +- B (matrix.hpp:121-134), contiguous records
 template <int L>
 void launch_addsub(const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N, int is_sub, int sh,
                    uint32_t* err, cudaStream_t st);
+
+// output slot per Strassen / Winograd child of a pre-addition (< 0: child not produced)
+struct ChildSlots {
+  int8_t s[7];
+};
 
 // Fast-algorithm level transforms (fastmm.hpp:133-219), batched over the nodes of
 // one recursion level.  Parents: nodes x (rows x cols) records (row-major, dense),
@@ -75,6 +84,10 @@ void launch_addsub(const uint32_t* A, const uint32_t* B, uint32_t* C, int64_t N,
 template <int L>
 void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
                    uint32_t* children, int sh, uint32_t* err, cudaStream_t st);
+// one node's pre-additions with the children placed by `slots` (L <= 32)
+template <int L>
+void launch_preadd_slots(int algo, int side, const uint32_t* parent, int rows, int cols, uint32_t* children,
+                         ChildSlots slots, int sh, cudaStream_t st);
 // Children products (7 per parent, hm x hn) -> parent C (rows x cols, stripped).
 // Optional trace output of Winograd's T1/T2 (2 x hm x hn per parent) when t_out != nullptr.
 // rowlist (device, optional): only these child rows [0, hm) are combined (and the parent rows

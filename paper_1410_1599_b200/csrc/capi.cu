@@ -1994,10 +1994,18 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       const char* e = std::getenv("MPGPU_LU_LOOKAHEAD");
       return !(e && e[0] == '0');
     }();
-    const int la_grid = [] {
+    const int la_grid_big = [] {
       const char* e = std::getenv("MPGPU_LU_LA_GRID");
       return e ? std::atoi(e) : 32;  // measured: 16 54.2, 32 52.1, 64 53.4, 148 58.3 ms (n=2048, K=64)
     }();
+    // once the rest of the Schur update is shorter than the look-ahead panel (the trailing
+    // matrix below ~1000 rows at 256 bits), the panel is the step's critical path: give it
+    // the whole grid
+    const int64_t la_switch = [] {
+      const char* e = std::getenv("MPGPU_LU_LA_SWITCH");
+      return e ? std::atoll(e) : (int64_t)0;
+    }();
+    auto la_grid_for = [&](int64_t rest) { return rest > la_switch ? la_grid_big : 0; };
     const bool lookahead = la_env && L <= 32;
     if (lookahead && !h->hi) {
       int lo = 0, hi_pr = 0;
@@ -2007,11 +2015,29 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_lp, cudaEventDisableTiming));
     }
     bool factored = false;  // the panel at `off` was already factored by the look-ahead
+    // MPGPU_LU_TRACE=1: per-step event times to stderr (diagnostics of the look-ahead overlap)
+    static const bool lu_trace = std::getenv("MPGPU_LU_TRACE") != nullptr;
+    struct Mark {
+      int64_t off;
+      const char* what;
+      cudaEvent_t e;
+    };
+    std::vector<Mark> tmarks;
+    auto tmark = [&](const char* what, cudaStream_t on) {
+      if (!lu_trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, on);
+      tmarks.push_back({off, what, e});
+    };
+    tmark("start", st);
     while (n - off > K) {
       const int64_t rest = n - off - K;
       if (!factored) panel_factor(off, K, st, 0);
+      tmark("panel(st)", st);
       panel_swap(off, K);
       mpg::launch_trsm_l_panel<L>(a, n, off, K, off + K, rest, sh, st);
+      tmark("swap+trsm", st);
       const uint32_t* l21 = a + ((off + K) * n + off) * S;
       const uint32_t* u12 = a + (off * n + off + K) * S;
       uint32_t* a22 = a + ((off + K) * n + off + K) * S;
@@ -2024,12 +2050,15 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
         SchurSplit<L> sp;
         int r = schur_part_a<L>(h, sp, kernel, n_min, l21, u12, a22, n, rest, K, K, sh, stats ? &ss : nullptr);
         if (r) return r;
+        tmark("part A", st);
         CUDA_TRY(h, cudaEventRecord(h->ev_la, st));
         CUDA_TRY(h, cudaStreamWaitEvent(h->hi, h->ev_la, 0));
-        panel_factor(off + K, K, h->hi, la_grid);
+        panel_factor(off + K, K, h->hi, la_grid_for(rest));
+        tmark("next panel(hi)", h->hi);
         CUDA_TRY(h, cudaEventRecord(h->ev_lp, h->hi));
         r = schur_part_b<L>(h, sp, kernel, n_min, l21, u12, a22, n, rest, K, K, sh, stats ? &sb : nullptr);
         if (r) return r;
+        tmark("part B", st);
         CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_lp, 0));
         factored = true;
       } else if (kernel == MPGPU_SIMPLE || kernel == MPGPU_BLOCK) {
@@ -2053,6 +2082,18 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
     }
     if (!factored) panel_factor(off, n - off, st, 0);
     panel_swap(off, n - off);
+    tmark("end", st);
+    if (lu_trace) {
+      cudaDeviceSynchronize();
+      float prev = 0;
+      for (const Mark& mk : tmarks) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tmarks[0].e, mk.e);
+        fprintf(stderr, "[lu] off %5lld %-15s %9.3f ms  (+%.3f)\n", (long long)mk.off, mk.what, ms, ms - prev);
+        prev = ms;
+      }
+      for (const Mark& mk : tmarks) cudaEventDestroy(mk.e);
+    }
     return 0;
   });
   if (stats) {

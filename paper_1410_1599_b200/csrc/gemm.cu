@@ -104,6 +104,26 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
 #define MPG_KK_UNROLL_8 2  // measured: 2 beats 1 and 4 at 256 bits (and loses at L >= 16)
 #endif
 
+#ifndef MPG_SADDR
+#define MPG_SADDR 1  // measured: leaf -1.4 % at 256 bits, neutral at 512 / 1024 (profiles/r02_ab_saddr.jsonl)
+#endif
+
+// record from shared memory (32-bit shared-window address): 16-byte vector loads
+template <int L>
+__device__ __forceinline__ void lds_rec(uint32_t addr, MP<L>& x) {
+  constexpr int S = rec_stride(L);
+  uint32_t w[S];
+#pragma unroll
+  for (int k = 0; k < S; k += 4)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[k]), "=r"(w[k + 1]), "=r"(w[k + 2]), "=r"(w[k + 3])
+                 : "r"(addr + 4 * k));
+#pragma unroll
+  for (int k = 0; k < L; ++k) x.m[k] = w[k];
+  x.e = (int32_t)w[L];
+  x.s = w[L + 1];
+}
+
 #ifndef MPG_TM_8
 #define MPG_TM_8 16
 #endif
@@ -261,6 +281,11 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
       const uint32_t* a_rows = sA + (kt & 1) * A_WORDS + ty * TK * S;
       const uint32_t* b_cols = sB + (kt & 1) * B_WORDS + tx * S;
       const int kend = min(TK, g.l - kt * TK);
+#if MPG_SADDR
+      // shared-window addresses carried through the k loop (two adds per step) instead of
+      // pointers the compiler rematerialises from the thread index every step
+      uint32_t sa_cur = smem_addr(a_rows), sb_cur = smem_addr(b_cols);
+#endif
 #pragma unroll GemmCfg<L>::KU
       for (int kk = 0; kk < kend; ++kk) {
         const int k = kt * TK + kk;
@@ -274,11 +299,19 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
         }
         const uint32_t* ar = a_rows + kk * S;
         MP<L> a;
+#if MPG_SADDR
+        if constexpr (!A_STREAM) lds_rec<L>(sa_cur, a);
+#else
         if constexpr (!A_STREAM) MPG_LOAD<L>(ar, a);
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           MP<L> b, t;
+#if MPG_SADDR
+          lds_rec<L>(sb_cur + u * TN * S * 4, b);
+#else
           MPG_LOAD<L>(b_cols + (kk * TNB + u * TN) * S, b);
+#endif
           const int32_t ae = A_STREAM ? (int32_t)ar[L] : a.e;
           const uint32_t as = A_STREAM ? ar[L + 1] : a.s;
           auto a_at = [&](int q) { return A_STREAM ? ar[q] : a.m[q]; };
@@ -297,6 +330,10 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
           mp_add<L>(pacc[u], t, 0u, g.sh, pacc[u]);
 #endif
         }
+#if MPG_SADDR
+        sa_cur += S * 4;
+        sb_cur += TNB * S * 4;
+#endif
       }
     }
     __syncthreads();

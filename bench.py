@@ -580,15 +580,16 @@ def lu_leg(args, P, torch, stream, flush, leaf_peak_tiops):
         ha, hf = pinned(A), pinned(A)
         e2e = []
         for rep in range(3):
+            # the factorisation is in place: restore the input outside the timed region
+            hf.limbs[:], hf.exp[:], hf.sign[:] = ha.limbs, ha.exp, ha.sign
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            work.upload(ha)
-            rc = PL.lib.mpgpu_lu_blocked(work._h, C.byref(work.m), K, int(P.Algorithm.winograd), nmin, 1,
-                                         piv.ctypes.data_as(C.c_void_p), C.byref(zp), None)
+            rc = PL.lib.mpgpu_lu_blocked_host(work._h, bits, n, hf.limbs.ctypes.data_as(C.c_void_p),
+                                              hf.exp.ctypes.data_as(C.c_void_p), hf.sign.ctypes.data_as(C.c_void_p),
+                                              hf.nlimbs, K, int(P.Algorithm.winograd), nmin, 1,
+                                              piv.ctypes.data_as(C.c_void_p), C.byref(zp), None)
             if rc:
-                raise RuntimeError(f"mpgpu_lu_blocked rc={rc}")
-            PL.lib.mpgpu_download(work._h, C.byref(work.m), hf.limbs.ctypes.data_as(C.c_void_p),
-                                  hf.exp.ctypes.data_as(C.c_void_p), hf.sign.ctypes.data_as(C.c_void_p), hf.nlimbs)
+                raise RuntimeError(f"mpgpu_lu_blocked_host rc={rc}")
             if rep:
                 e2e.append(time.perf_counter() - t0)
         e2e_ms = float(np.mean(e2e)) * 1e3
@@ -608,7 +609,7 @@ def lu_leg(args, P, torch, stream, flush, leaf_peak_tiops):
                "schur_leaf_roofline": {"achieved": schur_tiops, "peak": leaf_peak_tiops, "unit": "TIOP/s (IMAD-eq)",
                                        "frac": schur_tiops / leaf_peak_tiops},
                "madd_per_s": (n ** 3 / 3) / (float(np.mean(dev_ms)) * 1e-3),
-               "e2e": {"ms": e2e_ms, "api": "mpgpu_upload + mpgpu_lu_blocked + mpgpu_download, pinned host SoA, wall",
+               "e2e": {"ms": e2e_ms, "api": "mpgpu_lu_blocked_host (the drop-in's lu_blocked: transfers overlapped with the factorisation), pinned host SoA, wall",
                        "h2d_bytes": nbytes_soa(n * n, L), "d2h_bytes": nbytes_soa(n * n, L)},
                "solve_ms": solve_ms, "solve": "column-oriented lu_solve (exact=False)",
                "forward_error_max_rel": fwd, "forward_error": "max_rel_error_solution(x, 1) in MP on the device"}

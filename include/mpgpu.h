@@ -153,6 +153,15 @@ int mpgpu_vec_op(mpgpu_handle* h, int op, const mpgpu_mat* A, const mpgpu_mat* B
  * stats->mul/addsub accumulate the Schur multiply counts (schur_ops). */
 int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64_t n_min,
                      int pivoting, int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats);
+/* The same on an n x n matrix in HOST SoA buffers, factored in place (the drop-in's
+ * lu_blocked, blocklu.hpp:121-146, with the transfers overlapped: the first K columns are
+ * copied first, the rest while the first panel is factored, and each block of K rows is
+ * copied back as soon as no later step touches it).  Factors bit-identical to
+ * mpgpu_lu_blocked's; on an error the buffers' contents are unspecified.  Not to be run
+ * concurrently with other calls on the same handle. */
+int mpgpu_lu_blocked_host(mpgpu_handle* h, int32_t prec, int64_t n, uint32_t* limbs, int32_t* exp,
+                          uint8_t* sign, int32_t host_nlimbs, int64_t K, int kernel, int64_t n_min,
+                          int pivoting, int64_t* piv_out, int64_t* zero_pivot, mpgpu_stats* stats);
 /* Ly = Pb, Ux = y (blocklu.hpp:215-245); piv may be NULL (pivot-free factors).
  * exact = 1 replays the reference's summation order (bit-exact; the back
  * substitution is an O(n^2) serial chain of rounded adds); exact = 0 runs the

@@ -289,16 +289,14 @@ inline LUFactors lu_blocked(const Matrix& a, const BlockLUConfig& cfg, Precision
   mpgpu_handle* h = detail::handle();
   const auto n = static_cast<std::int64_t>(a.rows());
   detail::Soa sa = detail::to_soa(a);
-  mpgpu_mat da{};
   int kernel = static_cast<int>(cfg.kernel);  // mpmm::Algorithm order == MPGPU_* order
-  int rc = mpgpu_alloc_matrix(h, n, n, static_cast<std::int32_t>(a.bits()), &da);
-  if (!rc) rc = mpgpu_upload(h, &da, sa.limbs.data(), sa.exp.data(), sa.sign.data(), sa.L);
   std::int64_t zp = 0;
   mpgpu_stats st{};
-  if (!rc) rc = mpgpu_lu_blocked(h, &da, static_cast<std::int64_t>(cfg.block_size), kernel,
+  // factored in place in the SoA buffers (transfers overlapped with the factorisation when
+  // the buffers are page-locked)
+  int rc = mpgpu_lu_blocked_host(h, static_cast<std::int32_t>(a.bits()), n, sa.limbs.data(), sa.exp.data(),
+                                 sa.sign.data(), sa.L, static_cast<std::int64_t>(cfg.block_size), kernel,
                                  static_cast<std::int64_t>(cfg.n_min), 0, nullptr, &zp, &st);
-  if (!rc) rc = mpgpu_download(h, &da, sa.limbs.data(), sa.exp.data(), sa.sign.data(), sa.L);
-  mpgpu_free_matrix(h, &da);
   detail::check(rc, zp);
   if (schur_ops) {
     schur_ops->mul += st.mul;

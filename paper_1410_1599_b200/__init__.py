@@ -5,7 +5,7 @@ from .mpmm import (EXP_ZERO, Algorithm, BlockLUConfig, DeviceError, DeviceGroup,
                    DomainError, Error, FastMMConfig, FastMMResult, LUFactors, Matrix, OpCounter,
                    PrecisionContext, RecursionLevel, SingularError, Stats, TopTrace, add, algorithm_name,
                    block_mul, count_fast, count_simple, equal_values, fast_mul, gemm_host, gemm_into, handle, identical,
-                   lu_blocked, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
+                   lu_blocked, lu_blocked_host, lu_columnwise, lu_solve, mat_vec_mul, nlimbs_for, pad_even, parse_algorithm,
                    record_words, recursion_plan, set_device, set_stream, simple_mul, solve,
                    solve_columnwise, sub, vec_op, UndefinedMetricError, RelErrorStats, SolutionError,
                    max_rel_error, max_rel_error_solution, one_norm, convert, lu_solve_many,

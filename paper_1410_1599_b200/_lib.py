@@ -61,6 +61,8 @@ _SIGS = {
     "mpgpu_addsub": (C.c_int, [vp, C.c_int, MatP, MatP, MatP]),
     "mpgpu_vec_op": (C.c_int, [vp, C.c_int, MatP, MatP, MatP]),
     "mpgpu_lu_blocked": (C.c_int, [vp, MatP, C.c_int64, C.c_int, C.c_int64, C.c_int, vp, i64p, StatsP]),
+    "mpgpu_lu_blocked_host": (C.c_int, [vp, C.c_int32, C.c_int64, vp, vp, vp, C.c_int32, C.c_int64, C.c_int,
+                                        C.c_int64, C.c_int, vp, i64p, StatsP]),
     "mpgpu_lu_solve": (C.c_int, [vp, MatP, vp, MatP, MatP, C.c_int, i64p]),
     "mpgpu_matrix_view": (C.c_int, [MatP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, MatP]),
     "mpgpu_fast_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p]),

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <initializer_list>
 #include <mutex>
 #include <string>
@@ -20,6 +21,15 @@
 #include "../../include/mpgpu.h"
 #include "kernels.h"
 #include "mp_arith.cuh"
+
+// host-buffer LU (mpgpu_lu_blocked_host): hooks the factorisation calls so the PCIe
+// transfers overlap it -- the operand arrives in two column blocks, the factored rows
+// leave as soon as no later step touches them
+struct LuHostIO {
+  std::function<int()> before_panel0;  // columns [0, K) on the device
+  std::function<int()> before_swap0;   // the whole matrix on the device
+  std::function<int(int64_t, int64_t)> rows_final;  // rows [r0, r0 + nr) final
+};
 
 struct mpgpu_handle {
   int device = 0;
@@ -38,6 +48,7 @@ struct mpgpu_handle {
   // pipelined host GEMM: downloads on their own stream; per-quadrant events
   cudaStream_t dl = nullptr;
   cudaEvent_t pev[16] = {};
+  LuHostIO* lu_io = nullptr;  // set by mpgpu_lu_blocked_host for the duration of the call
 };
 
 namespace {
@@ -1041,6 +1052,20 @@ int download_async(mpgpu_handle* h, const uint32_t* rec, int L, int64_t N, uint3
 //   C21 = (t1 + m4) - m7 last.  Every element sees the reference's operation sequence:
 //   bit-identical to mpgpu_gemm.
 // ---------------------------------------------------------------------------
+// page-locked host memory (cudaMallocHost / cudaHostRegister): asynchronous copies to and
+// from pageable memory are synchronous for the host, which would serialise the pipelines
+static bool host_pinned(std::initializer_list<const void*> ps) {
+  for (const void* p : ps) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (a.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
 static bool host_pipe_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MPGPU_HOST_PIPE");
@@ -1536,7 +1561,7 @@ int mpgpu_gemm_host(mpgpu_handle* h, int algo, int64_t param, int32_t prec, int6
   if (rc) return rc;
   std::lock_guard<std::mutex> lk(h->mu);
   cudaSetDevice(h->device);
-  if (host_pipe_applies(algo, param, m, l, n, Lh, L)) {
+  if (host_pipe_applies(algo, param, m, l, n, Lh, L) && host_pinned({al, ae, as, bl, be, bs, cl, ce, cs})) {
     if (stats) {
       std::memset(stats, 0, sizeof *stats);
       uint64_t c[2];
@@ -2014,6 +2039,18 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_la, cudaEventDisableTiming));
       CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_lp, cudaEventDisableTiming));
     }
+    LuHostIO* io = h->lu_io;
+    bool swapped0 = false;  // the first interchange pass (it touches every column) has been issued
+    auto before_swap = [&]() -> int {
+      if (io && !swapped0 && io->before_swap0) {
+        swapped0 = true;
+        return io->before_swap0();
+      }
+      swapped0 = true;
+      return 0;
+    };
+    if (io && io->before_panel0)
+      if (int r = io->before_panel0()) return r;
     bool factored = false;  // the panel at `off` was already factored by the look-ahead
     // MPGPU_LU_TRACE=1: per-step event times to stderr (diagnostics of the look-ahead overlap)
     static const bool lu_trace = std::getenv("MPGPU_LU_TRACE") != nullptr;
@@ -2035,8 +2072,12 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       const int64_t rest = n - off - K;
       if (!factored) panel_factor(off, K, st, 0);
       tmark("panel(st)", st);
+      if (int r = before_swap()) return r;
       panel_swap(off, K);
       mpg::launch_trsm_l_panel<L>(a, n, off, K, off + K, rest, sh, st);
+      // rows [off, off + K) are final: later interchanges involve rows >= off + K only
+      if (io && io->rows_final)
+        if (int r = io->rows_final(off, K)) return r;
       tmark("swap+trsm", st);
       const uint32_t* l21 = a + ((off + K) * n + off) * S;
       const uint32_t* u12 = a + (off * n + off + K) * S;
@@ -2081,7 +2122,10 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
       off += K;
     }
     if (!factored) panel_factor(off, n - off, st, 0);
+    if (int r = before_swap()) return r;
     panel_swap(off, n - off);
+    if (io && io->rows_final)
+      if (int r = io->rows_final(off, n - off)) return r;
     tmark("end", st);
     if (lu_trace) {
       cudaDeviceSynchronize();
@@ -2151,6 +2195,143 @@ int lu_solve_impl(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const
   return rc;
 }
 }  // namespace
+
+// blocked LU from and to HOST SoA buffers (in place), the transfers overlapped with the
+// factorisation: columns [0, K) are copied first (the first panel needs only them), the
+// rest while that panel is factored; after step k's trsm rows [kK, (k+1)K) are final (every
+// later interchange involves rows >= (k+1)K) and are copied back while the factorisation
+// goes on.  Same kernels, same order: the factors are bit-identical to mpgpu_lu_blocked's.
+int mpgpu_lu_blocked_host(mpgpu_handle* h, int32_t prec, int64_t n, uint32_t* limbs, int32_t* exp, uint8_t* sign,
+                          int32_t host_nlimbs, int64_t K, int kernel, int64_t n_min, int pivoting, int64_t* piv_out,
+                          int64_t* zero_pivot, mpgpu_stats* stats) {
+  if (!h || !limbs || !exp || !sign) return MPGPU_ERR_DOMAIN;
+  if (zero_pivot) *zero_pivot = 0;
+  if (n < 1) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: matrix must be at least 1x1");
+  if (K == 0) return fail(h, MPGPU_ERR_DIMENSION, "lu_blocked: block size must be at least 1");
+  const int L = nlimbs_for(prec);
+  if (!L) return fail(h, MPGPU_ERR_DOMAIN, "precision %d outside the device range", prec);
+  if (host_nlimbs < (prec + 31) / 32) return fail(h, MPGPU_ERR_DOMAIN, "host limb count too small for precision");
+  int rc;
+  if (host_nlimbs != L || n <= 1 || !host_pipe_enabled() || !host_pinned({limbs, exp, sign})) {
+    // plain sequence: upload, factor, download
+    mpgpu_mat A{};
+    rc = mpgpu_alloc_matrix(h, n, n, prec, &A);
+    if (rc) return rc;
+    rc = mpgpu_upload(h, &A, limbs, exp, sign, host_nlimbs);
+    if (!rc) rc = mpgpu_lu_blocked(h, &A, K, kernel, n_min, pivoting, piv_out, zero_pivot, stats);
+    if (!rc) rc = mpgpu_download(h, &A, limbs, exp, sign, host_nlimbs);
+    mpgpu_free_matrix(h, &A);
+    return rc;
+  }
+  const int64_t K0 = std::min<int64_t>(K, n);
+  const size_t soa = sizeof(uint32_t) * L + sizeof(int32_t) + 1;
+  auto al256 = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t b0 = al256(soa * (size_t)(n * K0)), b1 = al256(soa * (size_t)(n * (n - K0)) + 1);
+  const size_t brec = al256(sizeof(uint32_t) * (size_t)rec_stride(L) * (size_t)(n * n));
+  const size_t total_bytes = brec + b0 + b1 + al256(soa * (size_t)(n * n));
+  // the device matrix and the SoA staging from the stream-ordered pool (no cudaMalloc /
+  // cudaFree, which synchronise, per call): records | column block 0 | the other columns |
+  // the factored rows
+  uint8_t* pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaSetDevice(h->device);
+    if (!h->aux) {
+      CUDA_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+    }
+    if (!h->dl) {
+      CUDA_TRY(h, cudaStreamCreateWithFlags(&h->dl, cudaStreamNonBlocking));
+      for (cudaEvent_t& e : h->pev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if ((rc = ensure_pool(h, total_bytes + total_bytes / 8))) return rc;
+    CUDA_TRY(h, cudaMallocAsync(reinterpret_cast<void**>(&pool), total_bytes, h->stream));
+  }
+  struct FreePool {
+    mpgpu_handle* h;
+    uint8_t* p;
+    ~FreePool() {
+      if (h->aux) cudaStreamSynchronize(h->aux);
+      if (h->dl) cudaStreamSynchronize(h->dl);
+      cudaFreeAsync(p, h->stream);
+      cudaStreamSynchronize(h->stream);
+    }
+  } free_pool{h, pool};
+  mpgpu_mat A{n, n, prec, L, reinterpret_cast<uint32_t*>(pool), n, 0};
+  uint8_t* stage = pool + brec;
+  cudaEvent_t up0 = h->pev[0], up1 = h->pev[1], ready = h->pev[12];
+  // the device matrix exists (allocated on the handle's stream) before the copies land
+  CUDA_TRY(h, cudaEventRecord(ready, h->stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->aux, ready, 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->dl, ready, 0));
+  struct Blk {
+    uint32_t* l;
+    int32_t* e;
+    uint8_t* s;
+  };
+  auto blk = [&](uint8_t* base, int64_t N) {
+    Blk b;
+    b.l = reinterpret_cast<uint32_t*>(base);
+    b.e = reinterpret_cast<int32_t*>(b.l + (size_t)L * N);
+    b.s = reinterpret_cast<uint8_t*>(b.e + N);
+    return b;
+  };
+  const Blk s0 = blk(stage, n * K0), s1 = blk(stage + b0, n * (n - K0)), sd = blk(stage + b0 + b1, n * n);
+  // copies in (aux stream): columns [c0, c0 + w) of every row into a dense n x w SoA block
+  auto copy_cols = [&](const Blk& d, int64_t c0, int64_t w, cudaEvent_t ev) -> int {
+    if (w <= 0) {
+      CUDA_TRY(h, cudaEventRecord(ev, h->aux));
+      return MPGPU_OK;
+    }
+    const int64_t N = n * w;
+    for (int j = 0; j < L; ++j)
+      CUDA_TRY(h, cudaMemcpy2DAsync(d.l + (size_t)j * N, sizeof(uint32_t) * w, limbs + (size_t)j * n * n + c0,
+                                    sizeof(uint32_t) * n, sizeof(uint32_t) * w, n, cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaMemcpy2DAsync(d.e, sizeof(int32_t) * w, exp + c0, sizeof(int32_t) * n, sizeof(int32_t) * w, n,
+                                  cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaMemcpy2DAsync(d.s, w, sign + c0, n, w, n, cudaMemcpyHostToDevice, h->aux));
+    CUDA_TRY(h, cudaEventRecord(ev, h->aux));
+    return MPGPU_OK;
+  };
+  if ((rc = copy_cols(s0, 0, K0, up0)) || (rc = copy_cols(s1, K0, n - K0, up1))) return rc;
+  // conversions on the factorisation's stream, just before the data is needed
+  auto convert = [&](const Blk& b, int64_t c0, int64_t w, cudaEvent_t ev) -> int {
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev, 0));
+    if (w <= 0) return MPGPU_OK;
+    return dispatch_store(L, [&](auto Lc) {
+      constexpr int LL = decltype(Lc)::value;
+      mpg::launch_soa2rec_2d<LL>(b.l, b.e, b.s, n, w, n * w, A.rec + c0 * rec_stride(LL), n, h->stream);
+      return 0;
+    });
+  };
+  LuHostIO io;
+  io.before_panel0 = [&]() { return convert(s0, 0, K0, up0); };
+  io.before_swap0 = [&]() { return convert(s1, K0, n - K0, up1); };
+  int nrow_ev = 0;
+  io.rows_final = [&](int64_t r0, int64_t nr) -> int {
+    cudaEvent_t ev = h->pev[2 + (nrow_ev++ % 10)];  // (each is waited on right after it is recorded)
+    CUDA_TRY(h, cudaEventRecord(ev, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->dl, ev, 0));
+    const int64_t N = nr * n, off = r0 * n;
+    dispatch_store(L, [&](auto Lc) {
+      constexpr int LL = decltype(Lc)::value;
+      mpg::launch_rec2soa<LL>(A.rec + off * rec_stride(LL), N, sd.l + off, sd.e + off, sd.s + off, n * n, h->dl);
+      return 0;
+    });
+    for (int j = 0; j < L; ++j)
+      CUDA_TRY(h, cudaMemcpyAsync(limbs + (size_t)j * n * n + off, sd.l + (size_t)j * n * n + off,
+                                  sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, h->dl));
+    CUDA_TRY(h, cudaMemcpyAsync(exp + off, sd.e + off, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, h->dl));
+    CUDA_TRY(h, cudaMemcpyAsync(sign + off, sd.s + off, N, cudaMemcpyDeviceToHost, h->dl));
+    return MPGPU_OK;
+  };
+  h->lu_io = &io;
+  rc = mpgpu_lu_blocked(h, &A, K, kernel, n_min, pivoting, piv_out, zero_pivot, stats);
+  h->lu_io = nullptr;
+  CUDA_TRY(h, cudaStreamSynchronize(h->dl));
+  return rc;
+}
 
 int mpgpu_lu_solve(mpgpu_handle* h, const mpgpu_mat* F, const int64_t* piv, const mpgpu_mat* b, mpgpu_mat* x,
                    int exact, int64_t* zero_pivot) {

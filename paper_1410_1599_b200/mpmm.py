@@ -783,6 +783,35 @@ def lu_blocked(a: Matrix, cfg: BlockLUConfig, ctx: PrecisionContext, schur_ops: 
     return LUFactors(n, packed, piv if pivoting else None)
 
 
+def lu_blocked_host(a: Matrix, cfg: BlockLUConfig, ctx: PrecisionContext, pivoting: bool = False,
+                    stats: Optional[Stats] = None, out: Optional[Matrix] = None) -> LUFactors:
+    """lu_blocked through mpgpu_lu_blocked_host: the factorisation of a host matrix with the
+    transfers overlapped (page-locked buffers; `out`, if given, receives the factors and may be
+    `a` itself).  Bit-identical to lu_blocked."""
+    if a.rows() != a.cols():
+        raise DimensionError("lu_blocked: matrix must be square")
+    if a.bits() != ctx.bits():
+        raise DomainError("lu_blocked: working context must match the matrix precision")
+    if cfg.block_size == 0:
+        raise DimensionError("lu_blocked: block size must be at least 1")
+    n = a.rows()
+    if out is None:
+        out = Matrix(n, n, a.ctx(), a.limbs.copy(), a.exp.copy(), a.sign.copy())
+    elif out is not a:
+        out.limbs[:], out.exp[:], out.sign[:] = a.limbs, a.exp, a.sign
+    h = handle()
+    piv = np.zeros(n, np.int64)
+    zp = C.c_int64(0)
+    st = _L.MpgpuStats()
+    rc = _L.lib.mpgpu_lu_blocked_host(h, a.bits(), n, _ptr(out.limbs), _ptr(out.exp), _ptr(out.sign), out.nlimbs,
+                                      cfg.block_size, int(cfg.kernel), cfg.n_min, 1 if pivoting else 0, _ptr(piv),
+                                      C.byref(zp), C.byref(st))
+    _raise(h, rc, zp.value)
+    if stats is not None:
+        stats.__dict__.update(Stats.of(st).__dict__)
+    return LUFactors(n, out, piv if pivoting else None)
+
+
 def lu_columnwise(a: Matrix) -> LUFactors:
     """blocklu.hpp:107-112 (== lu_blocked with K >= n)."""
     if a.rows() != a.cols():

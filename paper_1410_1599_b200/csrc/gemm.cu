@@ -213,8 +213,8 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     const int k0 = kt * TK;
     constexpr int CH = S / 4;
     if (full_tile(kt)) {
+      constexpr uint32_t ABYTES = TK * S * 4, BBYTES = TNB * S * 4;
       if (tid < 32) {
-        constexpr uint32_t ABYTES = TK * S * 4, BBYTES = TNB * S * 4;
         if (tid == 0) mbar_expect(&s_bar[buf], TM * ABYTES + TK * BBYTES);
         __syncwarp();
         for (int c = tid; c < TM + TK; c += 32) {

@@ -38,6 +38,7 @@ inline int blocks_for(int64_t n) {
 // Every row's multiplier is produced inside the CTA that uses it, so one launch
 // per column suffices (no grid-wide dependency between rows).
 constexpr int LU_RB = 8;
+
 __device__ __forceinline__ uint64_t mag_key(uint32_t e, uint32_t top) {
   return e == (uint32_t)EXP_ZERO ? 0ull : (((uint64_t)(e ^ 0x80000000u)) << 32) | top;
 }
@@ -630,11 +631,13 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
   constexpr int S = rec_stride(L);
   extern __shared__ __align__(16) uint32_t s_dyn[];
   uint32_t* s_mult = s_dyn;                                      // chunk records
-  int* s_perm = reinterpret_cast<int*>(s_dyn + chunk * S);        // logical row - p -> physical row - p
+  uint32_t* s_urow = s_dyn + chunk * S;                          // the pivot row right of the pivot: k records
+  int* s_perm = reinterpret_cast<int*>(s_urow + k * S);          // logical row - p -> physical row - p
   __shared__ uint64_t s_wk[NT / 32];
   __shared__ int64_t s_wi[NT / 32];
   __shared__ int s_wc[NT / 32];
   __shared__ int64_t s_piv;
+  __shared__ uint64_t s_gk;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t rows_all = row_end - p;
   const int64_t lo = p + (int64_t)blockIdx.x * chunk;
@@ -642,14 +645,8 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
   for (int64_t t = tid; t < rows_all; t += NT) s_perm[t] = (int)t;
   __syncthreads();
   auto phys = [&](int64_t i) -> int64_t { return p + s_perm[i - p]; };
-  auto candidates = [&](int64_t col, int64_t from) {
-    uint64_t bk = 0;
-    int64_t bi = INT64_MAX;
-    int bc = 0;
-    for (int64_t i = max(from, lo) + tid; i < hi; i += NT) {
-      const uint32_t* r = a + (phys(i) * n + col) * S;
-      piv_combine(bk, bi, bc, mag_key(r[L], r[L - 1]), i, 1);
-    }
+  // the CTA's best (key, first row, count) -> cand_*[blockIdx.x]
+  auto publish = [&](uint64_t bk, int64_t bi, int bc) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
@@ -670,6 +667,16 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
       cand_cnt[blockIdx.x] = (uint64_t)bc;
     }
     __syncthreads();
+  };
+  auto candidates = [&](int64_t col, int64_t from) {
+    uint64_t bk = 0;
+    int64_t bi = INT64_MAX;
+    int bc = 0;
+    for (int64_t i = max(from, lo) + tid; i < hi; i += NT) {
+      const uint32_t* r = a + (phys(i) * n + col) * S;
+      piv_combine(bk, bi, bc, mag_key(r[L], r[L - 1]), i, 1);
+    }
+    publish(bk, bi, bc);
   };
   candidates(p, p);
   grid.sync();
@@ -708,6 +715,7 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
         gi = r;
       }
       s_piv = gi;
+      s_gk = gk;
       // interchange logical rows d and r (every CTA does the same)
       const int tmp = s_perm[d - p];
       s_perm[d - p] = s_perm[gi - p];
@@ -716,14 +724,27 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
     }
     __syncthreads();
     const int64_t pd = phys(d);
-    // zero pivot: every CTA sees the same a_dd and stops (blocklu.hpp:46-47)
-    if (a[(pd * n + d) * S + L] == (uint32_t)EXP_ZERO) {
+    // zero pivot: every CTA sees the same (maximal) key and stops (blocklu.hpp:46-47); the
+    // key is 0 exactly for a zero value
+    if (s_gk == 0) {
       if (blockIdx.x == 0 && tid == 0) *zp = d + 1;
       return;
     }
     const int64_t r0 = max(d + 1, lo);
     const int64_t nr = hi - r0;
     if (nr > 0) {
+      const int64_t w = p + k - d - 1;
+      // the pivot row's values right of the pivot, for the rank-1 update: copied into shared
+      // memory asynchronously, in the shadow of the divisions
+      {
+        constexpr int CH = S / 4;
+        const uint32_t* urow = a + (pd * n + d + 1) * S;
+        for (int64_t t = tid; t < w * CH; t += NT) {
+          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s_urow + 4 * t));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(urow + 4 * t));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      }
       for (int64_t t = tid; t < nr; t += NT) {
         MP<L> piv_v, x, q;
         load_rec<L>(a + (pd * n + d) * S, piv_v);
@@ -733,13 +754,13 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
         store_rec<L>(xr, q);
         store_rec<L>(s_mult + t * S, q);
       }
+      asm volatile("cp.async.wait_all;\n" ::);
       __syncthreads();
-      const int64_t w = p + k - d - 1;
       for (int64_t t = tid; t < nr * w; t += NT) {
         const int64_t rr = t / w, j = d + 1 + t % w;
         MP<L> l, u, pr, x;
         load_rec<L>(s_mult + rr * S, l);
-        load_rec<L>(a + (pd * n + j) * S, u);
+        load_rec<L>(s_urow + (j - d - 1) * S, u);
         mp_mul<L>(l, u, sh, pr);
         uint32_t* xr = a + (phys(r0 + rr) * n + j) * S;
         load_rec<L>(xr, x);
@@ -747,6 +768,8 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
         store_rec<L>(xr, x);
       }
     }
+    // (measured slower: the next column's candidates taken from the update's registers (+0.3 %),
+    // two update items per thread in one straight-line body (+1.2 %))
     if (d + 1 < p + k) {
       __syncthreads();
       candidates(d + 1, d + 1);
@@ -919,17 +942,20 @@ int launch_lu_panel_coop(uint32_t* a, int64_t n, int64_t p, int64_t k, int64_t r
   if (smem > 16 * 1024) return -1;  // caller falls back to per-column kernels
   if (pivoting && rows <= 12288 && std::getenv("MPGPU_LU_PERM") == nullptr) {
     // one barrier per column: logical row table in shared memory (+ rows int32 words)
-    smem_attr_once((const void*)lu_panel_perm_kernel<L>, 16 * 1024 + 4 * 12288);
+    // multipliers (<= 16 KB) + the pivot row (k records) + the row table
+    const int kurow = (int)(sizeof(uint32_t) * S * k);
+    if (kurow > 48 * 1024) return -1;
+    smem_attr_once((const void*)lu_panel_perm_kernel<L>, 16 * 1024 + 48 * 1024 + 4 * 12288);
     static const int per_sm2 = [] {
       int v = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lu_panel_perm_kernel<L>, NT, 16 * 1024 + 4 * 12288);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lu_panel_perm_kernel<L>, NT, 16 * 1024 + 48 * 1024 + 4 * 12288);
       return v;
     }();
     int64_t g2 = std::min<int64_t>(grid, (int64_t)per_sm2 * dev_sms);
     if (g2 < 1) g2 = 1;
     int64_t ch = (rows + g2 - 1) / g2;
     if (sizeof(uint32_t) * S * (size_t)ch > 16 * 1024) return -1;
-    const size_t smem2 = sizeof(uint32_t) * S * (size_t)ch + sizeof(int) * (size_t)rows;
+    const size_t smem2 = sizeof(uint32_t) * S * (size_t)ch + (size_t)kurow + sizeof(int) * (size_t)rows;
     void* args2[] = {&a, &n, &p, &k, &row_end, &piv, &zp, (void*)&sh, &cand_key, &cand_idx, &cand_cnt, &ch};
     cudaError_t e2 = cudaLaunchCooperativeKernel((void*)lu_panel_perm_kernel<L>, dim3((unsigned)g2), dim3(NT), args2,
                                                  smem2, st);

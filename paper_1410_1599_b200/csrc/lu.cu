@@ -756,11 +756,13 @@ __global__ void __launch_bounds__(NT) lu_panel_perm_kernel(uint32_t* a, int64_t 
       }
       asm volatile("cp.async.wait_all;\n" ::);
       __syncthreads();
-      for (int64_t t = tid; t < nr * w; t += NT) {
-        const int64_t rr = t / w, j = d + 1 + t % w;
+      const int wi = (int)w, items = (int)(nr * w);  // (32-bit index arithmetic: nr * w < 2^31)
+      for (int t = tid; t < items; t += NT) {
+        const int rr = t / wi, jj = t - rr * wi;
+        const int64_t j = d + 1 + jj;
         MP<L> l, u, pr, x;
         load_rec<L>(s_mult + rr * S, l);
-        load_rec<L>(s_urow + (j - d - 1) * S, u);
+        load_rec<L>(s_urow + jj * S, u);
         mp_mul<L>(l, u, sh, pr);
         uint32_t* xr = a + (phys(r0 + rr) * n + j) * S;
         load_rec<L>(xr, x);

@@ -25,13 +25,16 @@
 #endif
 
 #ifndef MPG_MINB_8
-#define MPG_MINB_8 4
+#define MPG_MINB_8 8  // with 8 x 16 tiles and k-tile 12: 8 CTAs of 128 threads per SM (measured: -1.1 % at cfg2, -3.8 % on the cfg3 shape vs 4 x 256, 16 x 16, k-tile 16)
 #endif
 #define MPG_MINB_1 4
 #define MPG_MINB_2 4
 #define MPG_MINB_4 3
 #ifndef MPG_MINB_16
 #define MPG_MINB_16 6  // 80 registers: 6 CTAs of 128 threads per SM (measured best, 512-bit cfg)
+#endif
+#ifndef MPG_TK_16
+#define MPG_TK_16 8
 #endif
 #ifndef MPG_TM_32
 #define MPG_TM_32 8
@@ -125,11 +128,11 @@ __device__ __forceinline__ void lds_rec(uint32_t addr, MP<L>& x) {
 }
 
 #ifndef MPG_TM_8
-#define MPG_TM_8 16
+#define MPG_TM_8 8
 #endif
 
 #ifndef MPG_TK_8
-#define MPG_TK_8 16
+#define MPG_TK_8 12
 #endif
 
 #ifndef MPG_U_8
@@ -166,7 +169,7 @@ struct GemmCfg<8> {
 };
 template <>
 struct GemmCfg<16> {
-  static constexpr int MINB = MPG_MINB_16, TM = 8, TN = 16, TK = 8, U = 1;
+  static constexpr int MINB = MPG_MINB_16, TM = 8, TN = 16, TK = MPG_TK_16, U = 1;
   static constexpr int KU = 1;
 };
 template <>

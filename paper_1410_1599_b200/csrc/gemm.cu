@@ -40,7 +40,7 @@
 #define MPG_TM_32 8
 #endif
 #ifndef MPG_TK_32
-#define MPG_TK_32 2  // measured: 2 > 4 > 8 at 1024 bits
+#define MPG_TK_32 8  // round 2 (bulk-copied k-tiles): 8 < 6 < 4 < 2 at 1024 bits (68.2 / 68.2 / 68.4 / 70.1 ms leaf)
 #endif
 #ifndef MPG_MINB_32
 #define MPG_MINB_32 3  // 166 registers: 3 CTAs of 128 threads per SM (measured best, 1024-bit cfg)

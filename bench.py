@@ -247,7 +247,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.probe_world:
-        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": args.gpus}), flush=True)
+        # one write(2) per line: the ranks share stdout and print() may split the line and its newline
+        os.write(1, (json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": args.gpus}) + "\n").encode())
         return
     if args.impl == "reference":
         run_reference(args, rank)

@@ -64,7 +64,75 @@ struct MP {
 // 2 L^2 multiply instructions (lo + hi) on the FMA pipe; the compiler maps the
 // carries onto IADD3.X / IMAD.X.
 // ---------------------------------------------------------------------------
-#ifndef MPG_MUL_PTX_CHAINS
+#if MPG_WIDE
+#undef MPG_MUL_EO
+#define MPG_MUL_EO 0  // the wide formats loop over local-memory limbs: no PTX carry chains there
+#elif !defined(MPG_MUL_EO)
+#define MPG_MUL_EO 1
+#endif
+#if MPG_MUL_EO
+// Row-wise schoolbook on two sets of 64-bit column-pair accumulators: limb products a_i*b_j
+// with i+j even accumulate into the pairs (2k, 2k+1) of X, those with i+j odd into the
+// pairs (2k+1, 2k+2) of Y.  Within a row the products of one set tile consecutive pairs,
+// so the row is two carry chains of `mad.lo.cc` / `madc.hi.cc` pairs, each pair fused by
+// ptxas into ONE IMAD.WIDE.U32.X (64-bit product + 64-bit addend + carry in/out through a
+// predicate): one instruction per limb product, no separate carry adds.  The carry out of a
+// chain lands in the low limb of the next pair up, which until then has only received such
+// carries (< L of them: the chains' upper ends are nondecreasing in i), so that add cannot
+// overflow.  P = X + Y (one IADD3.X chain) at the end.  C0: lowest column kept
+// (0: full product; L-2: the short product of mul_high_g, limbs below C0 stay 0).
+template <int L>
+__device__ __forceinline__ void eo_chain(uint32_t (&acc)[2 * L + 2], uint32_t ai, const uint32_t (&b)[L],
+                                         int i, int js) {
+  if (js >= L) return;
+  asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.cc.u32 %1, %2, %3, %1;"
+               : "+r"(acc[i + js]), "+r"(acc[i + js + 1])
+               : "r"(ai), "r"(b[js]));
+MPG_UNROLL
+  for (int j = js + 2; j < L; j += 2)
+    asm volatile("madc.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.cc.u32 %1, %2, %3, %1;"
+                 : "+r"(acc[i + j]), "+r"(acc[i + j + 1])
+                 : "r"(ai), "r"(b[j]));
+  const int top = i + js + ((L - 1 - js) / 2) * 2 + 2;
+  if (top < 2 * L) asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[top]));
+}
+
+template <int L, int C0, class AG>
+__device__ __forceinline__ void mul_eo_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+  uint32_t X[2 * L + 2], Y[2 * L + 2];
+MPG_UNROLL
+  for (int k = 0; k < 2 * L + 2; ++k) X[k] = Y[k] = 0;
+MPG_UNROLL
+  for (int i = 0; i < L; ++i) {
+    const uint32_t ai = a_at(i);
+    const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
+    eo_chain<L>(X, ai, b, i, j0 + ((i + j0) & 1));        // i + j even
+    eo_chain<L>(Y, ai, b, i, j0 + (((i + j0) & 1) ^ 1));  // i + j odd
+  }
+MPG_UNROLL
+  for (int k = 0; k < C0; ++k) r[k] = 0;
+  if (C0 == 2 * L - 1) {
+    r[C0] = X[C0] + Y[C0];
+  } else {
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r[C0]) : "r"(X[C0]), "r"(Y[C0]));
+MPG_UNROLL
+    for (int k = C0 + 1; k < 2 * L - 1; ++k)
+      asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r[k]) : "r"(X[k]), "r"(Y[k]));
+    asm volatile("addc.u32 %0, %1, %2;" : "=r"(r[2 * L - 1]) : "r"(X[2 * L - 1]), "r"(Y[2 * L - 1]));
+  }
+}
+
+template <int L, class AG>
+__device__ __forceinline__ void mul_full_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+  if constexpr (L == 1) {
+    const uint64_t t = (uint64_t)a_at(0) * b[0];
+    r[0] = (uint32_t)t;
+    r[1] = (uint32_t)(t >> 32);
+  } else {
+    mul_eo_g<L, 0>(a_at, b, r);
+  }
+}
+#elif !defined(MPG_MUL_PTX_CHAINS)
 // Row-wise schoolbook on 64-bit partial sums: t = a_i*b_j + r[i+j] + carry never
 // overflows 64 bits, and maps onto one IMAD.WIDE.U32 (product + 64-bit addend)
 // plus ~1.3 ALU carry ops per limb product -- no half-rate IMAD.HI.
@@ -125,6 +193,12 @@ __device__ __forceinline__ void mul_full(const uint32_t (&a)[L], const uint32_t 
 // products instead of L^2 -- the mulhigh trick MPFR itself uses for mpfr_mul.
 template <int L, class AG>
 __device__ __forceinline__ void mul_high_g(AG a_at, const uint32_t (&b)[L], uint32_t (&r)[2 * L]) {
+#if MPG_MUL_EO
+  if constexpr (L >= 3) {
+    mul_eo_g<L, L - 2>(a_at, b, r);
+    return;
+  }
+#endif
 MPG_UNROLL
   for (int i = 0; i < 2 * L; ++i) r[i] = 0;
 MPG_UNROLL

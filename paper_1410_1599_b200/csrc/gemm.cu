@@ -31,7 +31,7 @@
 #define MPG_MINB_2 4
 #define MPG_MINB_4 3
 #ifndef MPG_MINB_16
-#define MPG_MINB_16 6  // 80 registers: 6 CTAs of 128 threads per SM (measured best, 512-bit cfg)
+#define MPG_MINB_16 5  // with the carry-chained product: 5 CTAs of 128 threads (96 registers) beat 6 (80, spilling) by 3.8 % at 512 bits (profiles/r02_ab_eo2.jsonl)
 #endif
 #ifndef MPG_TK_16
 #define MPG_TK_16 8

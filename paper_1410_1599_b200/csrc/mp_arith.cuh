@@ -70,6 +70,9 @@ struct MP {
 #elif !defined(MPG_MUL_EO)
 #define MPG_MUL_EO 1
 #endif
+#ifndef MPG_EO_SKIPC
+#define MPG_EO_SKIPC 1
+#endif
 #if MPG_MUL_EO
 // Row-wise schoolbook on two sets of 64-bit column-pair accumulators: limb products a_i*b_j
 // with i+j even accumulate into the pairs (2k, 2k+1) of X, those with i+j odd into the
@@ -82,9 +85,9 @@ struct MP {
 // overflow.  P = X + Y (one IADD3.X chain) at the end.  C0: lowest column kept
 // (0: full product; L-2: the short product of mul_high_g, limbs below C0 stay 0).
 template <int L>
-__device__ __forceinline__ void eo_chain(uint32_t (&acc)[2 * L + 2], uint32_t ai, const uint32_t (&b)[L],
-                                         int i, int js) {
-  if (js >= L) return;
+__device__ __forceinline__ int eo_chain(uint32_t (&acc)[2 * L + 2], uint32_t ai, const uint32_t (&b)[L],
+                                        int i, int js, int prev_top) {
+  if (js >= L) return prev_top;
   asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.cc.u32 %1, %2, %3, %1;"
                : "+r"(acc[i + js]), "+r"(acc[i + js + 1])
                : "r"(ai), "r"(b[js]));
@@ -94,7 +97,11 @@ MPG_UNROLL
                  : "+r"(acc[i + j]), "+r"(acc[i + j + 1])
                  : "r"(ai), "r"(b[j]));
   const int top = i + js + ((L - 1 - js) / 2) * 2 + 2;
-  if (top < 2 * L) asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[top]));
+  // The chain's last pair (top-2, top-1) holds a product of an earlier row only if that
+  // row's chain ended on the same pair (prev_top == top); otherwise it holds at most L
+  // carry counts and a*b + counts + carry-in < 2^64: no carry out, nothing to add.
+  if (top < 2 * L && (!MPG_EO_SKIPC || prev_top == top)) asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[top]));
+  return top;
 }
 
 template <int L, int C0, class AG>
@@ -102,12 +109,13 @@ __device__ __forceinline__ void mul_eo_g(AG a_at, const uint32_t (&b)[L], uint32
   uint32_t X[2 * L + 2], Y[2 * L + 2];
 MPG_UNROLL
   for (int k = 0; k < 2 * L + 2; ++k) X[k] = Y[k] = 0;
+  int xtop = -1, ytop = -1;  // upper ends of the previous row's chains (compile-time after unrolling)
 MPG_UNROLL
   for (int i = 0; i < L; ++i) {
     const uint32_t ai = a_at(i);
     const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
-    eo_chain<L>(X, ai, b, i, j0 + ((i + j0) & 1));        // i + j even
-    eo_chain<L>(Y, ai, b, i, j0 + (((i + j0) & 1) ^ 1));  // i + j odd
+    xtop = eo_chain<L>(X, ai, b, i, j0 + ((i + j0) & 1), xtop);        // i + j even
+    ytop = eo_chain<L>(Y, ai, b, i, j0 + (((i + j0) & 1) ^ 1), ytop);  // i + j odd
   }
 MPG_UNROLL
   for (int k = 0; k < C0; ++k) r[k] = 0;
@@ -196,23 +204,24 @@ __device__ __forceinline__ void mul_high_g(AG a_at, const uint32_t (&b)[L], uint
 #if MPG_MUL_EO
   if constexpr (L >= 3) {
     mul_eo_g<L, L - 2>(a_at, b, r);
-    return;
-  }
+  } else
 #endif
+  {
 MPG_UNROLL
-  for (int i = 0; i < 2 * L; ++i) r[i] = 0;
+    for (int i = 0; i < 2 * L; ++i) r[i] = 0;
 MPG_UNROLL
-  for (int i = 0; i < L; ++i) {
-    const uint32_t ai = a_at(i);
-    const int j0 = (L - 2 - i) > 0 ? (L - 2 - i) : 0;
-    uint32_t carry = 0;
+    for (int i = 0; i < L; ++i) {
+      const uint32_t ai = a_at(i);
+      const int j0 = (L - 2 - i) > 0 ? (L - 2 - i) : 0;
+      uint32_t carry = 0;
 MPG_UNROLL
-    for (int j = j0; j < L; ++j) {
-      const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
-      r[i + j] = (uint32_t)t;
-      carry = (uint32_t)(t >> 32);
+      for (int j = j0; j < L; ++j) {
+        const uint64_t t = (uint64_t)ai * b[j] + r[i + j] + carry;
+        r[i + j] = (uint32_t)t;
+        carry = (uint32_t)(t >> 32);
+      }
+      r[i + L] = carry;
     }
-    r[i + L] = carry;
   }
 }
 

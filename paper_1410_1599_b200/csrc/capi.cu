@@ -229,7 +229,7 @@ std::vector<Level> plan_levels(int64_t m, int64_t l, int64_t n, int64_t n_min) {
 }
 
 // ---- recursion depth per precision from measured leaf throughput (north star (2)) ----
-// B200 measurements (tools/leaf_table.py -> profiles/r02_leaf_table.jsonl): Winograd products with
+// B200 measurements (tools/leaf_table.py -> profiles/r02_leaf_table_eo.jsonl, re-measured with the carry-chained product): Winograd products with
 // 7^d leaves of s^3 (s = 16 .. 512) per limb count; the leaf kernel's MP multiply-adds per second and
 // the pre- / post-addition record bandwidth at that recursion level.  The leaf rate is flat for
 // s >= 32 and drops ~15 % at s = 16; the additions run at 2-4.5 TB/s.
@@ -242,14 +242,14 @@ struct LeafTab {
   double post[kTabSizes];  // post-add GB/s
 };
 constexpr LeafTab kLeafTab[] = {
-    {4, {1.061e11, 1.251e11, 1.243e11, 1.311e11, 1.314e11, 1.307e11}, {2264, 3960, 3541, 4777, 4447, 3898},
-     {2221, 4036, 3812, 4527, 4193, 3811}},
-    {8, {6.568e10, 7.472e10, 7.390e10, 7.713e10, 7.739e10, 7.683e10}, {2027, 3758, 3372, 4533, 4185, 3852},
-     {2024, 3614, 3478, 4213, 4020, 3607}},
-    {16, {2.742e10, 2.938e10, 2.931e10, 3.004e10, 3.013e10, 3.019e10}, {2246, 3668, 3300, 4211, 4003, 3694},
-     {2005, 2947, 2693, 3371, 3269, 2985}},
-    {32, {8.016e9, 8.391e9, 8.475e9, 8.636e9, 8.667e9, 8.687e9}, {1949, 2922, 2645, 3354, 3230, 3050},
-     {2170, 3213, 2923, 3743, 3557, 3284}},
+    {4, {1.286e11, 1.522e11, 1.496e11, 1.575e11, 1.576e11, 1.558e11}, {2180, 4261, 3841, 5167, 4859, 4259},
+     {2227, 4582, 4065, 5935, 5441, 4763}},
+    {8, {7.947e10, 9.115e10, 9.118e10, 9.462e10, 9.456e10, 9.441e10}, {2103, 3748, 3352, 4514, 4294, 3689},
+     {2230, 4380, 3903, 5518, 5135, 4459}},
+    {16, {3.653e10, 3.928e10, 3.894e10, 3.975e10, 3.969e10, 3.963e10}, {2259, 3496, 3174, 4071, 3814, 3465},
+     {2170, 3205, 2965, 3714, 3551, 3293}},
+    {32, {1.211e10, 1.271e10, 1.268e10, 1.289e10, 1.287e10, 1.286e10}, {1971, 3001, 2739, 3450, 3314, 3065},
+     {2277, 3491, 3161, 4060, 3840, 3482}},
 };
 
 // table row for L (L < 4: the 128-bit row; L > 32: the 1024-bit row with the rate scaled by (32/L)^2)

@@ -107,6 +107,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
 #define MPG_KK_UNROLL_8 2  // measured: 2 beats 1 and 4 at 256 bits (and loses at L >= 16)
 #endif
 
+#ifndef MPG_SH0_L
+#define MPG_SH0_L 8  // limb count whose p == 32 L case gets its own leaf instantiation (0: none)
+#endif
 #ifndef MPG_SADDR
 #define MPG_SADDR 1  // measured: leaf -1.4 % at 256 bits, neutral at 512 / 1024 (profiles/r02_ab_saddr.jsonl)
 #endif
@@ -178,8 +181,11 @@ struct GemmCfg<32> {
   static constexpr int KU = 1;
 };
 
-template <int L, int TM, int TN, int TK, int U, bool FOLD>
+template <int L, int TM, int TN, int TK, int U, bool FOLD, bool SH0 = false>
 __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(const GemmArgs g) {
+  // SH0: p == 32 L (no unused low bits) known at compile time -- the rounding position tests
+  // leave the multiply-add (measured at L = 8: leaf -3.1 %; at L = 16 / 32 it costs registers: +3 / +5 %)
+#define MPG_SH (SH0 ? 0 : g.sh)
   // FOLD: Block k-tiles (kb < l) -- a second accumulator and the C = RN(C + P) folds;
   // without them (Simple, Strassen / Winograd leaves, LU Schur) the result is P itself
   // (RN(-0 + P) == P), so acc and the per-step tile check are compiled out.
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
         if (FOLD && k == next_b) {  // Block k-tile boundary: C = RN(C + P), fresh P
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            mp_add<L>(acc[u], pacc[u], 0u, g.sh, acc[u]);
+            mp_add<L>(acc[u], pacc[u], 0u, MPG_SH, acc[u]);
             mp_zero(pacc[u], 1u);
           }
           next_b += g.kb;
@@ -322,15 +328,15 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
           // one zero test for the whole multiply-add: the product of nonzero operands is
           // nonzero, so with a nonzero accumulator neither primitive needs its own
           if (ae == EXP_ZERO || b.e == EXP_ZERO || pacc[u].e == EXP_ZERO) {
-            mp_mul_g<L>(a_at, ae, as, b, g.sh, t);
-            mp_add<L>(pacc[u], t, 0u, g.sh, pacc[u]);
+            mp_mul_g<L>(a_at, ae, as, b, MPG_SH, t);
+            mp_add<L>(pacc[u], t, 0u, MPG_SH, pacc[u]);
           } else {
-            mp_mul_g<L, decltype(a_at), true>(a_at, ae, as, b, g.sh, t);
-            mp_add<L, true>(pacc[u], t, 0u, g.sh, pacc[u]);
+            mp_mul_g<L, decltype(a_at), true>(a_at, ae, as, b, MPG_SH, t);
+            mp_add<L, true>(pacc[u], t, 0u, MPG_SH, pacc[u]);
           }
 #else
-          mp_mul_g<L>(a_at, ae, as, b, g.sh, t);
-          mp_add<L>(pacc[u], t, 0u, g.sh, pacc[u]);
+          mp_mul_g<L>(a_at, ae, as, b, MPG_SH, t);
+          mp_add<L>(pacc[u], t, 0u, MPG_SH, pacc[u]);
 #endif
         }
 #if MPG_SADDR
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     if (j >= g.n) break;
     MP<L> res;
     if constexpr (FOLD) {
-      mp_add<L>(acc[u], pacc[u], 0u, g.sh, res);
+      mp_add<L>(acc[u], pacc[u], 0u, MPG_SH, res);
     } else {
       res = pacc[u];
     }
@@ -357,12 +363,13 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
     if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
       MP<L> old;
       load_rec<L>(cr, old);
-      mp_add<L>(old, res, 1u, g.sh, res);
+      mp_add<L>(old, res, 1u, MPG_SH, res);
     }
     if (exp_out_of_range(res.e)) atomicOr(g.err, ERR_EXP_RANGE);
     store_rec<L>(cr, res);
   }
 }
+#undef MPG_SH
 
 // ---- warp-specialised leaf (L = 8, one k-tile: Simple, fast-algorithm leaves, LU Schur) ----
 // The multiply-add's two halves load different pipes: the product (43 IMAD.WIDE + its carry
@@ -570,6 +577,10 @@ void launch_tiles(const GemmArgs& g, cudaStream_t st) {
   }
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
   auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
+  if constexpr (L == MPG_SH0_L) {
+    if (g.sh == 0)
+      kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false, true>;
+  }
   smem_attr_once((const void*)kern, (int)smem);
   // grid.z is limited to 65535: deep recursions (7^d leaves) launch in batch chunks
   for (int z0 = 0; z0 < g.batch; z0 += 65535) {

@@ -119,12 +119,14 @@ MPG_UNROLL
   }
 MPG_UNROLL
   for (int k = 0; k < C0; ++k) r[k] = 0;
-  if (C0 == 2 * L - 1) {
-    r[C0] = X[C0] + Y[C0];
-  } else {
-    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r[C0]) : "r"(X[C0]), "r"(Y[C0]));
+  // limb C0 belongs to one set only (X when C0 is even, Y when odd): the carry chain starts above it
+  r[C0] = (C0 & 1) ? Y[C0] : X[C0];
+  if (C0 + 1 == 2 * L - 1) {
+    r[C0 + 1] = X[C0 + 1] + Y[C0 + 1];
+  } else if (C0 + 1 < 2 * L - 1) {
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r[C0 + 1]) : "r"(X[C0 + 1]), "r"(Y[C0 + 1]));
 MPG_UNROLL
-    for (int k = C0 + 1; k < 2 * L - 1; ++k)
+    for (int k = C0 + 2; k < 2 * L - 1; ++k)
       asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r[k]) : "r"(X[k]), "r"(Y[k]));
     asm volatile("addc.u32 %0, %1, %2;" : "=r"(r[2 * L - 1]) : "r"(X[2 * L - 1]), "r"(Y[2 * L - 1]));
   }

@@ -107,8 +107,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t* sdst, const uint32_t* gsrc, u
 #define MPG_KK_UNROLL_8 2  // measured: 2 beats 1 and 4 at 256 bits (and loses at L >= 16)
 #endif
 
-#ifndef MPG_SH0_L
-#define MPG_SH0_L 8  // limb count whose p == 32 L case gets its own leaf instantiation (0: none)
+#ifndef MPG_SH0_SPEC
+// limb counts whose p == 32 L case gets its own leaf instantiation (measured: leaf -7.2 % at
+// 128 bits, -3.4 % at 256; +3 % / +5 % at 512 / 1024, where it costs registers)
+#define MPG_SH0_SPEC(L) ((L) == 4 || (L) == 8)
 #endif
 #ifndef MPG_SADDR
 #define MPG_SADDR 1  // measured: leaf -1.4 % at 256 bits, neutral at 512 / 1024 (profiles/r02_ab_saddr.jsonl)
@@ -184,7 +186,7 @@ struct GemmCfg<32> {
 template <int L, int TM, int TN, int TK, int U, bool FOLD, bool SH0 = false>
 __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(const GemmArgs g) {
   // SH0: p == 32 L (no unused low bits) known at compile time -- the rounding position tests
-  // leave the multiply-add (measured at L = 8: leaf -3.1 %; at L = 16 / 32 it costs registers: +3 / +5 %)
+  // leave the multiply-add (MPG_SH0_SPEC)
 #define MPG_SH (SH0 ? 0 : g.sh)
   // FOLD: Block k-tiles (kb < l) -- a second accumulator and the C = RN(C + P) folds;
   // without them (Simple, Strassen / Winograd leaves, LU Schur) the result is P itself
@@ -577,7 +579,7 @@ void launch_tiles(const GemmArgs& g, cudaStream_t st) {
   }
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
   auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
-  if constexpr (L == MPG_SH0_L) {
+  if constexpr (MPG_SH0_SPEC(L)) {
     if (g.sh == 0)
       kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false, true>;
   }

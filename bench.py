@@ -122,6 +122,13 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def issued_imad_eq_per_madd(L, bits):
+    """IMAD-equivalents the leaf issues per multiply-add: the short product (mp_arith.cuh mul_high_g)
+    when the precision fills its limbs, the full product otherwise."""
+    products = (L * L + 3 * L - 2) // 2 if (bits == 32 * L and L >= 3) else L * L
+    return 2 * products
+
+
 def measured_peaks():
     try:
         return json.loads(PEAKS_FILE.read_text())
@@ -332,6 +339,11 @@ def main():
             "peak_basis": f"{IMAD_PER_CLK_PER_SM} IMAD/clk/SM x {sms} SMs x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
     if clocks.get("sm_mhz"):
         roof["frac_at_measured_clock"] = achieved / (IMAD_PER_CLK_PER_SM * sms * clocks["sm_mhz"] * 1e6 / 1e12)
+    # the kernel issues the SHORT product when p == 32 L ((L^2 + 3L - 2)/2 limb products, one
+    # IMAD.WIDE.U32 = 2 IMAD-eq each): the share of the IMAD pipe those issued products hold
+    issued = issued_imad_eq_per_madd(L, args.bits)
+    roof["issued_imad_eq_per_madd"] = issued
+    roof["frac_issued"] = roof["frac"] * issued / (2 * L * L)
 
     line = {
         "metric": "MP mul-adds/s (n^3/t, classical-equivalent)", "value": value, "unit": "madd/s",
@@ -698,6 +710,7 @@ def precision_sweep(args, P, torch, peak_tiops):
         achieved = st.leaf_madds * 2 * L * L / (leaf * 1e-3) / 1e12
         out[str(bits)] = {"leaf_ms": leaf, "leaf_madds": st.leaf_madds, "imad_eq_per_madd": 2 * L * L,
                           "achieved_tiops": achieved, "frac": achieved / peak_tiops,
+                          "frac_issued": achieved / peak_tiops * issued_imad_eq_per_madd(L, bits) / (2 * L * L),
                           "device_ms_at_n_min": min(P.gemm_into(algo, param, da, db, dc).device_ms for _ in range(2))}
         if algo in (P.Algorithm.strassen, P.Algorithm.winograd):
             # the cutoff chosen per precision from the measured leaf throughput (MPGPU_AUTO_NMIN)

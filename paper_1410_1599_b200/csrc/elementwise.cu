@@ -24,6 +24,30 @@
 
 namespace mpg {
 
+// resident CTAs per SM asked of the compiler (register cap) for the fused level transforms.
+// Measured (profiles/r02_ab_ew.jsonl, n = 1024 Winograd): at 512 bits 2 CTAs instead of 1 take the
+// pre-additions 1.35 -> 1.20 ms and the post-additions 0.68 -> 0.50 ms; at 256 bits 3 or 4 CTAs
+// (80 / 64 registers, spilling) lose 7 %, at 1024 bits 2 CTAs lose 7 % (pre) / 32 % (post)
+#ifndef MPG_PRE_MINB_8
+#define MPG_PRE_MINB_8 2
+#endif
+#ifndef MPG_POST_MINB_8
+#define MPG_POST_MINB_8 2
+#endif
+#ifndef MPG_PRE_MINB_16
+#define MPG_PRE_MINB_16 2
+#endif
+#ifndef MPG_POST_MINB_16
+#define MPG_POST_MINB_16 2
+#endif
+#ifndef MPG_PRE_MINB_32
+#define MPG_PRE_MINB_32 1
+#endif
+#ifndef MPG_POST_MINB_32
+#define MPG_POST_MINB_32 1
+#endif
+constexpr int pre_minb(int L) { return L <= 8 ? MPG_PRE_MINB_8 : L <= 16 ? MPG_PRE_MINB_16 : L <= 32 ? MPG_PRE_MINB_32 : 1; }
+constexpr int post_minb(int L) { return L <= 8 ? MPG_POST_MINB_8 : L <= 16 ? MPG_POST_MINB_16 : L <= 32 ? MPG_POST_MINB_32 : 1; }
 namespace {
 constexpr int NT = 256;
 inline int grid_for(int64_t n) {
@@ -140,7 +164,7 @@ __device__ __forceinline__ void load_padded(const uint32_t* P, int rows, int col
 // after it, so at most two MP values plus the adder's window are live -- the
 // 1024-bit instantiation stays in registers.
 template <int L>
-__global__ void preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
+__global__ void __launch_bounds__(256, pre_minb(L)) preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
                               int rows, int cols, uint32_t* __restrict__ children, int sh, ChildSlots slots) {
   constexpr int S = rec_stride(L);
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
@@ -285,7 +309,7 @@ __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r,
 }
 
 template <int L>
-__global__ void postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
+__global__ void __launch_bounds__(256, post_minb(L)) postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
                                int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
                                int sh, uint32_t* err, const int* __restrict__ rowlist, int nrows, int cc0,
                                int ncc, const uint64_t* __restrict__ rowtab) {

@@ -373,210 +373,14 @@ __global__ void __launch_bounds__(TM* TN, GemmCfg<L>::MINB) gemm_leaf_kernel(con
 }
 #undef MPG_SH
 
-// ---- warp-specialised leaf (L = 8, one k-tile: Simple, fast-algorithm leaves, LU Schur) ----
-// The multiply-add's two halves load different pipes: the product (43 IMAD.WIDE + its carry
-// chain) the FMA-heavy pipe, the aligned / normalised / rounded add the ALU pipe.  In the
-// one-role kernel every warp alternates between them and both pipes idle a third of the time
-// (profiles/r02_leaf_pipe_accounting.json).  Here the CTA's first TM*TN threads ("producers")
-// form the rounded products RN(a_ik b_kj) and the other TM*TN ("accumulators") fold them into
-// RN(acc + t) in k order, so each scheduler always holds warps of both kinds.  Products pass
-// through a ring of R shared-memory slots (one record per output per k), handed over with
-// named barriers: FULL[s] = 2 + s (producers arrive, accumulators wait), EMPTY[s] = 2 + R + s
-// (accumulators arrive once they hold the record, producers wait before refilling).
-// Every output sees the same operations in the same order as gemm_leaf_kernel: bit-identical.
-#ifndef MPG_WS_8
-#define MPG_WS_8 0  // measured: leaf 9.19 vs 7.50 ms at cfg2 (profiles/r02_ab_ws.jsonl)
-#endif
-#ifndef MPG_WS_R
-#define MPG_WS_R 4
-#endif
-#ifndef MPG_WS_MINB
-#define MPG_WS_MINB 4
-#endif
-
-__device__ __forceinline__ void bar_sync_n(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-template <int L>
-__device__ __forceinline__ void sts_rec(uint32_t addr, const MP<L>& x) {
-  constexpr int S = rec_stride(L);
-  uint32_t w[S];
-#pragma unroll
-  for (int k = 0; k < L; ++k) w[k] = x.m[k];
-  w[L] = (uint32_t)x.e;
-  w[L + 1] = x.s;
-#pragma unroll
-  for (int k = L + 2; k < S; ++k) w[k] = 0;
-#pragma unroll
-  for (int k = 0; k < S; k += 4)
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr + 4 * k), "r"(w[k]), "r"(w[k + 1]),
-                 "r"(w[k + 2]), "r"(w[k + 3])
-                 : "memory");
-}
-
-template <int L, int TM, int TN, int TK, int R>
-__global__ void __launch_bounds__(2 * TM* TN, MPG_WS_MINB) gemm_leaf_ws_kernel(const GemmArgs g) {
-  static_assert(2 + 2 * R <= 16, "named barriers");
-  constexpr int S = rec_stride(L);
-  constexpr int NT = TM * TN;  // producers == accumulators == outputs of the tile
-  constexpr int A_WORDS = TM * TK * S, B_WORDS = TK * TN * S, P_WORDS = NT * S;
-  extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* sA = smem;
-  uint32_t* sB = smem + 2 * A_WORDS;
-  uint32_t* sP = sB + 2 * B_WORDS;
-  __shared__ __align__(8) uint64_t s_bar[2];
-
-  const bool producer = threadIdx.x < NT;
-  const int tid = producer ? threadIdx.x : threadIdx.x - NT;
-  const int tx = tid % TN, ty = tid / TN;
-  const int z = blockIdx.z;
-  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
-  const uint32_t* A = g.A + (int64_t)z * g.strideA * S;
-  const uint32_t* B = g.B + (int64_t)z * g.strideB * S;
-  const int KT = (g.l + TK - 1) / TK;
-  const int i = i0 + ty;
-  const bool active = (i < g.m) && (j0 + tx < g.n);
-  const uint32_t p_addr = smem_addr(sP) + tid * S * 4;
-
-  if (threadIdx.x == 0) {
-    mbar_init1(&s_bar[0]);
-    mbar_init1(&s_bar[1]);
-  }
-  __syncthreads();
-
-  if (producer) {
-    uint32_t bar_phase = 0;
-    auto full_tile = [&](int kt) {
-      const int k0 = kt * TK;
-      return MPG_BULK && i0 + TM <= g.m && j0 + TN <= g.n && k0 + TK <= g.l;
-    };
-    auto stage = [&](int kt, int buf) {
-      const int k0 = kt * TK;
-      constexpr int CH = S / 4;
-      if (full_tile(kt)) {
-        constexpr uint32_t ABYTES = TK * S * 4, BBYTES = TN * S * 4;
-        if (tid < 32) {
-          if (tid == 0) mbar_expect(&s_bar[buf], TM * ABYTES + TK * BBYTES);
-          __syncwarp();
-          for (int c = tid; c < TM + TK; c += 32) {
-            if (c < TM)
-              bulk_g2s(sA + buf * A_WORDS + c * TK * S, A + ((int64_t)(i0 + c) * g.lda + k0) * S, ABYTES,
-                       &s_bar[buf]);
-            else
-              bulk_g2s(sB + buf * B_WORDS + (c - TM) * TN * S, B + ((int64_t)(k0 + c - TM) * g.ldb + j0) * S,
-                       BBYTES, &s_bar[buf]);
-          }
-        }
-        return;
-      }
-#pragma unroll 1
-      for (int c = tid; c < TM * TK * CH; c += NT) {
-        const int e = c / CH, w = c - e * CH;
-        const int r = e / TK, kk = e - r * TK;
-        const int gi = i0 + r, gk = k0 + kk;
-        const bool ok = gi < g.m && gk < g.l;
-        const uint32_t* src = A + ((int64_t)(ok ? gi : 0) * g.lda + (ok ? gk : 0)) * S + 4 * w;
-        cp_async16(sA + buf * A_WORDS + e * S + 4 * w, src, ok ? 16 : 0);
-      }
-#pragma unroll 1
-      for (int c = tid; c < TK * TN * CH; c += NT) {
-        const int e = c / CH, w = c - e * CH;
-        const int kk = e / TN, cc = e - kk * TN;
-        const int gk = k0 + kk, gj = j0 + cc;
-        const bool ok = gk < g.l && gj < g.n;
-        const uint32_t* src = B + ((int64_t)(ok ? gk : 0) * g.ldb + (ok ? gj : 0)) * S + 4 * w;
-        cp_async16(sB + buf * B_WORDS + e * S + 4 * w, src, ok ? 16 : 0);
-      }
-    };
-    stage(0, 0);
-    cp_async_commit();
-    int it = 0;
-    for (int kt = 0; kt < KT; ++kt) {
-      if (kt + 1 < KT) stage(kt + 1, (kt + 1) & 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-      if (full_tile(kt)) {
-        const int b = kt & 1;
-        mbar_wait_parity(&s_bar[b], (bar_phase >> b) & 1u);
-        bar_phase ^= 1u << b;
-      }
-      bar_sync_n(1, NT);
-      uint32_t sa_cur = smem_addr(sA + (kt & 1) * A_WORDS + ty * TK * S);
-      uint32_t sb_cur = smem_addr(sB + (kt & 1) * B_WORDS + tx * S);
-      const int kend = min(TK, g.l - kt * TK);
-#pragma unroll 1
-      for (int kk = 0; kk < kend; ++kk, ++it) {
-        const int slot = it % R;
-        if (it >= R) bar_sync_n(2 + R + slot, 2 * NT);
-        if (active) {
-          MP<L> a, b, t;
-          lds_rec<L>(sa_cur, a);
-          lds_rec<L>(sb_cur, b);
-          mp_mul_g<L>([&](int q) { return a.m[q]; }, a.e, a.s, b, g.sh, t);
-          sts_rec<L>(p_addr + slot * P_WORDS * 4, t);
-        }
-        bar_arrive_n(2 + slot, 2 * NT);
-        sa_cur += S * 4;
-        sb_cur += TN * S * 4;
-      }
-      bar_sync_n(1, NT);
-    }
-    return;
-  }
-
-  // accumulators: RN(acc + t) in k order, then the epilogue
-  MP<L> acc;
-  mp_zero(acc, 1u);
-#pragma unroll 1
-  for (int it = 0; it < g.l; ++it) {
-    const int slot = it % R;
-    bar_sync_n(2 + slot, 2 * NT);
-    MP<L> t;
-    if (active) lds_rec<L>(p_addr + slot * P_WORDS * 4, t);
-    if (it + R < g.l) bar_arrive_n(2 + R + slot, 2 * NT);
-    if (active) mp_add<L>(acc, t, 0u, g.sh, acc);
-  }
-  if (!active) return;
-  const int j = j0 + tx;
-  uint32_t* C = g.C + (int64_t)z * g.strideC * S;
-  uint32_t* cr = g.rowtab ? reinterpret_cast<uint32_t*>(g.rowtab[i]) + ((g.batch0 + z) * g.strideC + j) * S
-                          : C + ((int64_t)i * g.ldc + j) * S;
-  MP<L> res = acc;
-  if (g.sub_from_c) {  // LU Schur update: A22 = RN(A22 - prod) (blocklu.hpp:138-141)
-    MP<L> old;
-    load_rec<L>(cr, old);
-    mp_add<L>(old, res, 1u, g.sh, res);
-  }
-  if (exp_out_of_range(res.e)) atomicOr(g.err, ERR_EXP_RANGE);
-  store_rec<L>(cr, res);
-}
+// (A warp-specialised L = 8 leaf -- producer warps forming the rounded products, accumulator warps
+// folding them in k order through a shared-memory ring -- was bit-exact but 22 % slower: leaf
+// 9.19 vs 7.50 ms at cfg2, profiles/r02_ab_ws.jsonl, r02_leaf8_ws_summary.json.  Removed.)
 
 template <int L, int TM, int TN>
 void launch_tiles(const GemmArgs& g, cudaStream_t st) {
   constexpr int TK = GemmCfg<L>::TK, U = GemmCfg<L>::U;
   constexpr int S = rec_stride(L);
-  if constexpr (L == 8 && U == 1 && MPG_WS_8) {
-    if (!(g.kb < g.l)) {
-      constexpr int R = MPG_WS_R;
-      const size_t smem = sizeof(uint32_t) * (2 * (TM * TK * S + TK * TN * S) + R * TM * TN * S);
-      auto kern = gemm_leaf_ws_kernel<L, TM, TN, TK, R>;
-      smem_attr_once((const void*)kern, (int)smem);
-      for (int z0 = 0; z0 < g.batch; z0 += 65535) {
-        GemmArgs gz = g;
-        gz.batch = std::min(65535, g.batch - z0);
-        gz.A += (int64_t)z0 * g.strideA * S;
-        gz.B += (int64_t)z0 * g.strideB * S;
-        gz.C += (int64_t)z0 * g.strideC * S;
-        gz.batch0 = g.batch0 + z0;
-        dim3 grid((g.n + TN - 1) / TN, (g.m + TM - 1) / TM, gz.batch);
-        kern<<<grid, 2 * TM * TN, smem, st>>>(gz);
-      }
-      return;
-    }
-  }
   const size_t smem = sizeof(uint32_t) * 2 * (TM * TK * S + TK * TN * U * S);
   auto kern = g.kb < g.l ? gemm_leaf_kernel<L, TM, TN, TK, U, true> : gemm_leaf_kernel<L, TM, TN, TK, U, false>;
   if constexpr (MPG_SH0_SPEC(L)) {

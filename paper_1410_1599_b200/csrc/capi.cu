@@ -2028,7 +2028,7 @@ int mpgpu_lu_blocked(mpgpu_handle* h, mpgpu_mat* A, int64_t K, int kernel, int64
     // the whole grid
     const int64_t la_switch = [] {
       const char* e = std::getenv("MPGPU_LU_LA_SWITCH");
-      return e ? std::atoll(e) : (int64_t)0;
+      return e ? std::atoll(e) : (int64_t)768;  // measured (n=2048 @256, K=64): 0 43.91, 512 43.73, 768 43.44, 1024 44.09 ms
     }();
     auto la_grid_for = [&](int64_t rest) { return rest > la_switch ? la_grid_big : 0; };
     const bool lookahead = la_env && L <= 32;

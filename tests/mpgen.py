@@ -114,3 +114,35 @@ def tie_cases(L: int, bits: int):
         s = np.array([i[2] for i in items], np.uint8)
         return m, e, s
     return pack(xs), pack(ys)
+
+
+def carry_patterns(L: int, bits: int) -> np.ndarray:
+    """(L, P) mantissas that maximise / isolate the carries of the limb-product chains:
+    all ones, a single saturated limb at every position, alternating saturated limbs, ..."""
+    cols = []
+    full = np.full(L, 0xFFFFFFFF, np.uint64)
+    cols.append(full.copy())
+    cols.append(np.full(L, 0xFFFFFFFE, np.uint64))
+    top = np.zeros(L, np.uint64)
+    top[L - 1] = 0x80000000
+    cols.append(top.copy())
+    t = full.copy()
+    t[L - 1] = 0x80000000
+    cols.append(t)
+    t = np.zeros(L, np.uint64)
+    t[L - 1] = 0xFFFFFFFF
+    cols.append(t)
+    for par in (0, 1):
+        t = np.zeros(L, np.uint64)
+        t[par::2] = 0xFFFFFFFF
+        cols.append(t)
+    for k in range(L):
+        t = np.zeros(L, np.uint64)
+        t[k] = 0xFFFFFFFF
+        cols.append(t)
+        t = full.copy()
+        t[k] = 0
+        cols.append(t)
+    m = np.stack(cols, axis=1).astype(np.uint32)
+    m[L - 1] |= np.uint32(0x80000000)
+    return clear_below(m, bits)

@@ -4,7 +4,7 @@ the signs of zeros, on structured edge cases at every supported limb count."""
 import numpy as np
 import pytest
 
-from mpgen import structured_pairs, tie_cases
+from mpgen import carry_patterns, structured_pairs, tie_cases
 
 PRECS = [2, 17, 32, 33, 53, 64, 100, 128, 150, 200, 255, 256, 300, 512, 777, 1000, 1024]
 
@@ -36,6 +36,31 @@ def test_ops_match_mpfr(P, O, bits):
             want = O.vec_op(3, a3, b3)
         else:
             want = O.vec_op(op, a, b)
+        bad = ~((got.exp == want.exp) & (got.sign == want.sign) & np.all(got.limbs == want.limbs, axis=0))
+        assert not bad.any(), f"op {op} bits {bits}: {int(bad.sum())} mismatches, first at {np.argmax(bad)}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [64, 100, 128, 200, 256, 500, 512, 1000, 1024])
+def test_mul_carry_extremes(P, O, bits):
+    """Every pair of carry-saturating mantissas (all ones, one saturated limb at each position,
+    alternating limbs, ...): the product's carry chains (mp_arith.cuh mul_eo_g, short and full
+    product) against mpfr_mul, and the same operands through add / sub."""
+    ctx = P.PrecisionContext(bits)
+    L = max(1, (bits + 31) // 32)
+    pat = carry_patterns(L, bits)
+    npat = pat.shape[1]
+    ia, ib = np.meshgrid(np.arange(npat), np.arange(npat), indexing="ij")
+    xm, ym = pat[:, ia.ravel()], pat[:, ib.ravel()]
+    n = xm.shape[1]
+    rng = np.random.default_rng(bits)
+    xe = rng.integers(-5, 5, size=n).astype(np.int64)
+    ye = xe - rng.integers(0, 3, size=n)
+    xs = rng.integers(0, 2, size=n).astype(np.uint8)
+    ys = rng.integers(0, 2, size=n).astype(np.uint8)
+    a, b = _mats(P, ctx, L, (xm, xe, xs), (ym, ye, ys))
+    for op in (2, 0, 1):
+        got, want = P.vec_op(op, a, b), O.vec_op(op, a, b)
         bad = ~((got.exp == want.exp) & (got.sign == want.sign) & np.all(got.limbs == want.limbs, axis=0))
         assert not bad.any(), f"op {op} bits {bits}: {int(bad.sum())} mismatches, first at {np.argmax(bad)}"
 

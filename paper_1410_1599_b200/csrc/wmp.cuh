@@ -13,6 +13,9 @@
 // Replaces, for the wide formats only, the thread-per-element primitives whose 1 KB
 // mantissas live in local memory (latency-bound, one element per thread).
 #pragma once
+#ifndef MPG_WMUL_FUSED
+#define MPG_WMUL_FUSED 1
+#endif
 #include <cstdint>
 
 #include "mp_arith.cuh"
@@ -450,10 +453,18 @@ __device__ __forceinline__ void product_w(const W<V>& x, const W<V>& y, const Sc
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint32_t bv = sc.b[40 + t - i - u];
+#if MPG_WMUL_FUSED
+        // product + 64-bit accumulate + carry-out in one IMAD.WIDE.U32 (ptxas fuses the
+        // mad.lo.cc / madc.hi.cc pair), then the third word: 2 instructions per limb product
+        asm volatile("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+                     : "+r"(acc[u][0]), "+r"(acc[u][1]), "+r"(acc[u][2])
+                     : "r"(av[u]), "r"(bv));
+#else
         const uint64_t pr = (uint64_t)av[u] * bv;
         asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[u][0]) : "r"((uint32_t)pr));
         asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[u][1]) : "r"((uint32_t)(pr >> 32)));
         asm volatile("addc.u32 %0, %0, 0;" : "+r"(acc[u][2]));
+#endif
       }
     }
 #pragma unroll

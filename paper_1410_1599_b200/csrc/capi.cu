@@ -327,6 +327,15 @@ int choose_nmin(int L, int64_t m, int64_t l, int64_t n, int64_t* n_min, int* dep
   return MPGPU_OK;
 }
 
+// two recursion levels of pre-additions per launch (MPGPU_PREADD_FUSE=0 disables; =N: up to N limbs)
+bool preadd_fuse_for(int L) {
+  static const int maxl = [] {
+    const char* e = std::getenv("MPGPU_PREADD_FUSE");
+    return e ? std::atoi(e) : 32;
+  }();
+  return L <= maxl;
+}
+
 int check_err(mpgpu_handle* h) {
   flush_timers();
   uint32_t e = 0;
@@ -576,20 +585,47 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
         if (lev > 0) op[lev].release();
         return 0;
       };
-      if (b_ready) {
-        for (int lev = 0, nd = 1; lev < d; ++lev, nd *= 7)
-          if (int rc = side_level(0, lev, nd)) return rc;
-        wait_b();
-        for (int lev = 0, nd = 1; lev < d; ++lev, nd *= 7)
-          if (int rc = side_level(1, lev, nd)) return rc;
-        for (int lev = 0; lev < d; ++lev) nodes *= 7;
-      } else {
-        for (int lev = 0; lev < d; ++lev) {
-          if (int rc = side_level(0, lev, nodes)) return rc;
-          if (int rc = side_level(1, lev, nodes)) return rc;
-          nodes *= 7;
+      // two levels per launch where the fused kernel exists (the intermediate level -- 7/4 of
+      // the parents written and read back -- stays in shared memory; same operands bit for bit)
+      auto side_level2 = [&](int side, int lev, int64_t nd) -> int {
+        const Level& P = lv[lev];
+        const Level& Q = lv[lev + 2];
+        std::vector<DevBuf>& op = side == 0 ? opA : opB;
+        const uint32_t* src = lev == 0 ? (side == 0 ? pa : pb) : op[lev].u32();
+        const int64_t rr = side == 0 ? P.m : P.l, cc = side == 0 ? P.l : P.n;
+        const int64_t qr = side == 0 ? Q.m : Q.l, qc = side == 0 ? Q.l : Q.n;
+        CUDA_TRY(h, op[lev + 2].alloc(h, sizeof(uint32_t) * S * nd * 49 * qr * qc));
+        if (!mpg::launch_preadd2<L>(algo, side, src, nd, (int)rr, (int)cc, op[lev + 2].u32(), sh, st)) return -1;
+        ++launches;
+        if (lev > 0) op[lev].release();
+        return 0;
+      };
+      auto side_all = [&](int side) -> int {
+        int64_t nd = 1;
+        for (int lev = 0; lev < d;) {
+          // an odd number of levels: the single one first (the deepest levels move the most bytes)
+          if (preadd_fuse_for(L) && lev + 2 <= d && (d - lev) % 2 == 0) {
+            const int rc = side_level2(side, lev, nd);
+            if (rc > 0) return rc;
+            if (rc == 0) {
+              lev += 2;
+              nd *= 49;
+              continue;
+            }
+            (side == 0 ? opA : opB)[lev + 2].release();  // no fused kernel for this limb count
+          }
+          if (int rc = side_level(side, lev, nd)) return rc;
+          lev += 1;
+          nd *= 7;
         }
-      }
+        return 0;
+      };
+      // the pre-additions of one side never read the other's: all A levels run first
+      // (overlapping B's upload when b_ready is set)
+      if (int rc = side_all(0)) return rc;
+      wait_b();
+      if (int rc = side_all(1)) return rc;
+      for (int lev = 0; lev < d; ++lev) nodes *= 7;
       a0.release();
       b0.release();
       if (stats) tpre.stop(&stats->preadd_ms);
@@ -607,23 +643,33 @@ int run_gemm(mpgpu_handle* h, int algo, int64_t param, const uint32_t* A, int64_
       opB[d].release();
       Timer tpost(timing, st);
       DevBuf top;
-      for (int lev = d - 1; lev >= 0; --lev) {
-        nodes /= 7;
-        const Level& P = lv[lev];
+      for (int lev = d - 1; lev >= 0;) {
+        // two levels per launch where the fused kernel exists: the products of level lev + 1
+        // combined straight into level lev - 1 (the level between them stays in shared memory)
+        const bool two = lev >= 1 && preadd_fuse_for(L) && mpg::has_postadd2(L);
+        const int tl = two ? lev - 1 : lev;
+        nodes /= two ? 49 : 7;
+        const Level& P = lv[tl];
         uint32_t* dst;
-        if (lev == 0 && ldc == n && !sub_from_c) {
+        if (tl == 0 && ldc == n && !sub_from_c) {
           dst = C;
-        } else if (lev == 0) {
+        } else if (tl == 0) {
           CUDA_TRY(h, top.alloc(h, sizeof(uint32_t) * S * m * n));
           dst = top.u32();
         } else {
-          CUDA_TRY(h, prod[lev].alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
-          dst = prod[lev].u32();
+          CUDA_TRY(h, prod[tl].alloc(h, sizeof(uint32_t) * S * nodes * P.m * P.n));
+          dst = prod[tl].u32();
         }
-        mpg::launch_postadd<L>(algo, prod[lev + 1].u32(), nodes, (int)P.m, (int)P.n, dst, nullptr, sh,
-                               h->d_err, st);
+        if (two) {
+          if (!mpg::launch_postadd2<L>(algo, prod[lev + 1].u32(), nodes, (int)P.m, (int)P.n, dst, sh, h->d_err, st))
+            return fail(h, MPGPU_ERR_DOMAIN, "internal: no fused post-addition for this limb count");
+        } else {
+          mpg::launch_postadd<L>(algo, prod[lev + 1].u32(), nodes, (int)P.m, (int)P.n, dst, nullptr, sh,
+                                 h->d_err, st);
+        }
         ++launches;
         prod[lev + 1].release();
+        lev = tl - 1;
       }
       if (top.p) {
         if (sub_from_c) {

@@ -46,6 +46,9 @@ namespace mpg {
 #ifndef MPG_POST_MINB_32
 #define MPG_POST_MINB_32 1
 #endif
+#ifndef MPG_ADD2_PT
+#define MPG_ADD2_PT 32  // positions per CTA of the fused two-level transforms (4 PT threads)
+#endif
 constexpr int pre_minb(int L) { return L <= 8 ? MPG_PRE_MINB_8 : L <= 16 ? MPG_PRE_MINB_16 : L <= 32 ? MPG_PRE_MINB_32 : 1; }
 constexpr int post_minb(int L) { return L <= 8 ? MPG_POST_MINB_8 : L <= 16 ? MPG_POST_MINB_16 : L <= 32 ? MPG_POST_MINB_32 : 1; }
 namespace {
@@ -160,9 +163,82 @@ __device__ __forceinline__ void load_padded(const uint32_t* P, int rows, int col
     mp_zero(x, 0);
 }
 
+// The level transform of one quadrant element: ld(q, x) reads quadrant q (0: 11, 1: 12, 2: 21,
+// 3: 22) of the virtually zero-padded parent, put(child, x) writes child operand `child`.
 // Each sum is formed from operands (re)loaded right before it and stored right
 // after it, so at most two MP values plus the adder's window are live -- the
 // 1024-bit instantiation stays in registers.
+template <int L, class LD, class PUT>
+__device__ __forceinline__ void preadd_body(int algo, int side, int sh, LD ld, PUT put) {
+  auto sum = [&](int qa, int qb, uint32_t neg, int child) {
+    MP<L> x, y;
+    ld(qa, x);
+    ld(qb, y);
+    mp_add<L>(x, y, neg, sh, x);
+    put(child, x);
+  };
+  auto copy = [&](int q, int child) {
+    MP<L> x;
+    ld(q, x);
+    put(child, x);
+  };
+  if (algo == 3) {
+    if (side == 0) {
+      // S1 = a21+a22 (M5), S2 = S1-a11 (M1), S3 = a11-a21 (M4), S4 = a12-S2 (M6)
+      MP<L> s1, s2, x;
+      ld(2, s1);
+      ld(3, x);
+      mp_add<L>(s1, x, 0u, sh, s1);
+      put(4, s1);
+      ld(0, x);
+      mp_add<L>(s1, x, 1u, sh, s2);
+      put(0, s2);
+      ld(1, x);
+      mp_add<L>(x, s2, 1u, sh, x);
+      put(5, x);
+      sum(0, 2, 1u, 3);
+      copy(0, 1);  // M2 = a11*b11
+      copy(1, 2);  // M3 = a12*b21
+      copy(3, 6);  // M7 = a22*S8
+    } else {
+      // S5 = b12-b11 (M5), S6 = b22-S5 (M1), S7 = b22-b12 (M4), S8 = S6-b21 (M7)
+      MP<L> s5, s6, x;
+      ld(1, s5);
+      ld(0, x);
+      mp_add<L>(s5, x, 1u, sh, s5);
+      put(4, s5);
+      ld(3, x);
+      mp_add<L>(x, s5, 1u, sh, s6);
+      put(0, s6);
+      ld(2, x);
+      mp_add<L>(s6, x, 1u, sh, x);
+      put(6, x);
+      sum(3, 1, 1u, 3);
+      copy(0, 1);  // b11
+      copy(2, 2);  // b21
+      copy(3, 5);  // b22
+    }
+  } else {
+    if (side == 0) {  // a11+a22, a21+a22, a11, a22, a11+a12, a21-a11, a12-a22
+      sum(0, 3, 0u, 0);
+      sum(2, 3, 0u, 1);
+      copy(0, 2);
+      copy(3, 3);
+      sum(0, 1, 0u, 4);
+      sum(2, 0, 1u, 5);
+      sum(1, 3, 1u, 6);
+    } else {  // b11+b22, b11, b12-b22, b21-b11, b22, b11+b12, b21+b22
+      sum(0, 3, 0u, 0);
+      copy(0, 1);
+      sum(1, 3, 1u, 2);
+      sum(2, 0, 1u, 3);
+      copy(3, 4);
+      sum(0, 1, 0u, 5);
+      sum(2, 3, 0u, 6);
+    }
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(256, pre_minb(L)) preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
                               int rows, int cols, uint32_t* __restrict__ children, int sh, ChildSlots slots) {
@@ -197,73 +273,69 @@ __global__ void __launch_bounds__(256, pre_minb(L)) preadd_kernel(int algo, int 
     auto put = [&](int child, const MP<L>& x) {
       if (slots.s[child] >= 0) store_rec<L>(out + slots.s[child] * cs, x);
     };
-    auto sum = [&](int qa, int qb, uint32_t neg, int child) {
-      MP<L> x, y;
-      ld(qa, x);
-      ld(qb, y);
-      mp_add<L>(x, y, neg, sh, x);
-      put(child, x);
-    };
-    auto copy = [&](int q, int child) {
-      MP<L> x;
-      ld(q, x);
-      put(child, x);
-    };
-    if (algo == 3) {
-      if (side == 0) {
-        // S1 = a21+a22 (M5), S2 = S1-a11 (M1), S3 = a11-a21 (M4), S4 = a12-S2 (M6)
-        MP<L> s1, s2, x;
-        ld(2, s1);
-        ld(3, x);
-        mp_add<L>(s1, x, 0u, sh, s1);
-        put(4, s1);
-        ld(0, x);
-        mp_add<L>(s1, x, 1u, sh, s2);
-        put(0, s2);
-        ld(1, x);
-        mp_add<L>(x, s2, 1u, sh, x);
-        put(5, x);
-        sum(0, 2, 1u, 3);
-        copy(0, 1);  // M2 = a11*b11
-        copy(1, 2);  // M3 = a12*b21
-        copy(3, 6);  // M7 = a22*S8
-      } else {
-        // S5 = b12-b11 (M5), S6 = b22-S5 (M1), S7 = b22-b12 (M4), S8 = S6-b21 (M7)
-        MP<L> s5, s6, x;
-        ld(1, s5);
-        ld(0, x);
-        mp_add<L>(s5, x, 1u, sh, s5);
-        put(4, s5);
-        ld(3, x);
-        mp_add<L>(x, s5, 1u, sh, s6);
-        put(0, s6);
-        ld(2, x);
-        mp_add<L>(s6, x, 1u, sh, x);
-        put(6, x);
-        sum(3, 1, 1u, 3);
-        copy(0, 1);  // b11
-        copy(2, 2);  // b21
-        copy(3, 5);  // b22
-      }
-    } else {
-      if (side == 0) {  // a11+a22, a21+a22, a11, a22, a11+a12, a21-a11, a12-a22
-        sum(0, 3, 0u, 0);
-        sum(2, 3, 0u, 1);
-        copy(0, 2);
-        copy(3, 3);
-        sum(0, 1, 0u, 4);
-        sum(2, 0, 1u, 5);
-        sum(1, 3, 1u, 6);
-      } else {  // b11+b22, b11, b12-b22, b21-b11, b22, b11+b12, b21+b22
-        sum(0, 3, 0u, 0);
-        copy(0, 1);
-        sum(1, 3, 1u, 2);
-        sum(2, 0, 1u, 3);
-        copy(3, 4);
-        sum(0, 1, 0u, 5);
-        sum(2, 3, 0u, 6);
+    preadd_body<L>(algo, side, sh, ld, put);
+  }
+}
+
+// Two recursion levels of the pre-additions in one launch: the 49 grandchildren of every node
+// straight from the node, the 7 children (the intermediate level: 7/4 of the node written and
+// read again) staying in shared memory.  A CTA owns PT consecutive positions (r2, c2) of the
+// grandchild grid of one node.  Phase 1: task (s, pos) -- s = (i2, j2), the sub-quadrant of the
+// children -- applies the level transform to the node's four quadrant elements at that
+// position and leaves the 7 children's values in shared memory (+0 where the position lies in
+// the children's zero padding: pad_operand, fastmm.hpp:91-97).  Phase 2: task (c1, pos) applies
+// the same transform to child c1's four sub-quadrant values and stores the 7 grandchildren.
+// Same per-element operation sequence as two preadd_kernel launches: bit-identical.
+template <int L, int PT>
+__global__ void __launch_bounds__(4 * PT) preadd2_kernel(int algo, int side, const uint32_t* __restrict__ parent,
+                                                        int64_t nodes, int rows, int cols,
+                                                        uint32_t* __restrict__ grand, int sh) {
+  constexpr int S = rec_stride(L);
+  extern __shared__ __align__(16) uint32_t s_v[];  // [c1][s][pos] records
+  const int hr1 = (rows + rows % 2) / 2, hc1 = (cols + cols % 2) / 2;
+  const int hr2 = (hr1 + hr1 % 2) / 2, hc2 = (hc1 + hc1 % 2) / 2;
+  const int64_t per2 = (int64_t)hr2 * hc2;
+  const int64_t tiles_per_node = (per2 + PT - 1) / PT;
+  const int64_t ntiles = tiles_per_node * nodes;
+  const int tid = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t node = tile / tiles_per_node;
+    const int64_t e0 = (tile - node * tiles_per_node) * PT;
+    const uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    {  // phase 1: 4 PT tasks, one per thread
+      const int s = tid / PT, pos = tid - s * PT;
+      const int64_t e = e0 + pos;
+      if (e < per2) {
+        const int r2 = (int)(e / hc2), c2 = (int)(e - (int64_t)r2 * hc2);
+        const int r1 = r2 + (s >> 1) * hr2, c1 = c2 + (s & 1) * hc2;  // position inside the children
+        uint32_t* v = s_v + ((int64_t)s * PT + pos) * S;
+        auto put = [&](int child, const MP<L>& x) { store_rec<L>(v + (int64_t)child * 4 * PT * S, x); };
+        if (r1 < hr1 && c1 < hc1) {
+          auto ld = [&](int q, MP<L>& x) {
+            load_padded<L>(P, rows, cols, r1 + (q >> 1) * hr1, c1 + (q & 1) * hc1, x);
+          };
+          preadd_body<L>(algo, side, sh, ld, put);
+        } else {  // the children's own zero padding (odd child dimension)
+          MP<L> z;
+          mp_zero(z, 0);
+#pragma unroll
+          for (int child = 0; child < 7; ++child) put(child, z);
+        }
       }
     }
+    __syncthreads();
+    // phase 2: 7 PT tasks over 4 PT threads
+    for (int task = tid; task < 7 * PT; task += 4 * PT) {
+      const int c1 = task / PT, pos = task - c1 * PT;
+      const int64_t e = e0 + pos;
+      if (e >= per2) continue;
+      const uint32_t* v = s_v + ((int64_t)c1 * 4 * PT + pos) * S;
+      auto ld = [&](int q, MP<L>& x) { load_rec<L>(v + (int64_t)q * PT * S, x); };
+      uint32_t* out = grand + (((node * 7 + c1) * 7) * per2 + e) * S;
+      auto put = [&](int child, const MP<L>& x) { store_rec<L>(out + (int64_t)child * per2 * S, x); };
+      preadd_body<L>(algo, side, sh, ld, put);
+    }
+    __syncthreads();
   }
 }
 
@@ -308,6 +380,78 @@ __device__ __forceinline__ void store_if(uint32_t* P, int rows, int cols, int r,
   }
 }
 
+// The combine of one quadrant element: ldc(k, x) reads child product k (0..6), put(q, x) writes
+// quadrant q (0: C11, 1: C12, 2: C21, 3: C22) of the parent, tt(t1, t2) sees Winograd's T1 / T2.
+template <int L, class LDC, class PUT, class TT>
+__device__ __forceinline__ void postadd_body(int algo, int sh, LDC ldc, PUT put, TT tt) {
+  if (algo == 3) {
+    // T1 = M1+M2, T2 = T1+M4; C11 = M2+M3, C12 = (T1+M5)+M6, C21 = T2-M7, C22 = T2+M5
+    MP<L> m1, m2, t1, t2, u, v;
+    ldc(0, m1);
+    ldc(1, m2);
+    mp_add<L>(m1, m2, 0u, sh, t1);
+    {
+      MP<L> m4;
+      ldc(3, m4);
+      mp_add<L>(t1, m4, 0u, sh, t2);
+    }
+    tt(t1, t2);
+    {
+      MP<L> m3;
+      ldc(2, m3);
+      mp_add<L>(m2, m3, 0u, sh, u);
+      put(0, u);
+    }
+    MP<L> m5;
+    ldc(4, m5);
+    {
+      MP<L> m6;
+      ldc(5, m6);
+      mp_add<L>(t1, m5, 0u, sh, u);
+      mp_add<L>(u, m6, 0u, sh, v);
+      put(1, v);
+    }
+    {
+      MP<L> m7;
+      ldc(6, m7);
+      mp_add<L>(t2, m7, 1u, sh, u);
+      put(2, u);
+    }
+    mp_add<L>(t2, m5, 0u, sh, u);
+    put(3, u);
+  } else {
+    // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
+    MP<L> p1, p4, p5, u, v;
+    ldc(0, p1);
+    ldc(3, p4);
+    ldc(4, p5);
+    mp_add<L>(p1, p4, 0u, sh, u);
+    mp_add<L>(u, p5, 1u, sh, v);
+    {
+      MP<L> p7;
+      ldc(6, p7);
+      mp_add<L>(v, p7, 0u, sh, u);
+      put(0, u);
+    }
+    MP<L> p3;
+    ldc(2, p3);
+    mp_add<L>(p3, p5, 0u, sh, u);
+    put(1, u);
+    MP<L> p2;
+    ldc(1, p2);
+    mp_add<L>(p2, p4, 0u, sh, u);
+    put(2, u);
+    mp_add<L>(p1, p3, 0u, sh, u);
+    mp_add<L>(u, p2, 1u, sh, v);
+    {
+      MP<L> p6;
+      ldc(5, p6);
+      mp_add<L>(v, p6, 0u, sh, u);
+      put(3, u);
+    }
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(256, post_minb(L)) postadd_kernel(int algo, const uint32_t* __restrict__ children, int64_t nodes, int rows,
                                int cols, uint32_t* __restrict__ parent, uint32_t* __restrict__ t_out,
@@ -344,75 +488,75 @@ __global__ void __launch_bounds__(256, post_minb(L)) postadd_kernel(int algo, co
       else
         load_rec<L>(M + k * cs, x);
     };
-    if (algo == 3) {
-      // T1 = M1+M2, T2 = T1+M4; C11 = M2+M3, C12 = (T1+M5)+M6, C21 = T2-M7, C22 = T2+M5
-      MP<L> m1, m2, t1, t2, u, v;
-      ldc(0, m1);
-      ldc(1, m2);
-      mp_add<L>(m1, m2, 0u, sh, t1);
-      {
-        MP<L> m4;
-        ldc(3, m4);
-        mp_add<L>(t1, m4, 0u, sh, t2);
-      }
+    auto put = [&](int q, const MP<L>& x) {
+      store_if<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x, err, rowtab, node);
+    };
+    auto tt = [&](const MP<L>& t1, const MP<L>& t2) {
       if (t_out) {
         store_rec<L>(t_out + (node * 2 * per + e) * S, t1);
         store_rec<L>(t_out + (node * 2 * per + per + e) * S, t2);
       }
-      {
-        MP<L> m3;
-        ldc(2, m3);
-        mp_add<L>(m2, m3, 0u, sh, u);
-        store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
-      }
-      MP<L> m5;
-      ldc(4, m5);
-      {
-        MP<L> m6;
-        ldc(5, m6);
-        mp_add<L>(t1, m5, 0u, sh, u);
-        mp_add<L>(u, m6, 0u, sh, v);
-        store_if<L>(P, rows, cols, r, c + hc, v, err, rowtab, node);
-      }
-      {
-        MP<L> m7;
-        ldc(6, m7);
-        mp_add<L>(t2, m7, 1u, sh, u);
-        store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
-      }
-      mp_add<L>(t2, m5, 0u, sh, u);
-      store_if<L>(P, rows, cols, r + hr, c + hc, u, err, rowtab, node);
-    } else {
-      // C11 = ((P1+P4)-P5)+P7, C12 = P3+P5, C21 = P2+P4, C22 = ((P1+P3)-P2)+P6
-      MP<L> p1, p4, p5, u, v;
-      ldc(0, p1);
-      ldc(3, p4);
-      ldc(4, p5);
-      mp_add<L>(p1, p4, 0u, sh, u);
-      mp_add<L>(u, p5, 1u, sh, v);
-      {
-        MP<L> p7;
-        ldc(6, p7);
-        mp_add<L>(v, p7, 0u, sh, u);
-        store_if<L>(P, rows, cols, r, c, u, err, rowtab, node);
-      }
-      MP<L> p3;
-      ldc(2, p3);
-      mp_add<L>(p3, p5, 0u, sh, u);
-      store_if<L>(P, rows, cols, r, c + hc, u, err, rowtab, node);
-      MP<L> p2;
-      ldc(1, p2);
-      mp_add<L>(p2, p4, 0u, sh, u);
-      store_if<L>(P, rows, cols, r + hr, c, u, err, rowtab, node);
-      mp_add<L>(p1, p3, 0u, sh, u);
-      mp_add<L>(u, p2, 1u, sh, v);
-      {
-        MP<L> p6;
-        ldc(5, p6);
-        mp_add<L>(v, p6, 0u, sh, u);
-        store_if<L>(P, rows, cols, r + hr, c + hc, u, err, rowtab, node);
+    };
+    postadd_body<L>(algo, sh, ldc, put, tt);
+  }
+}
+
+// Two recursion levels of the post-additions in one launch (the mirror of preadd2_kernel): the
+// node's C straight from its 49 grandchildren products, the 7 children products staying in
+// shared memory.  Phase 1: task (c1, pos) combines the 7 grandchildren of child c1 at position
+// pos = (r2, c2) into the child's four sub-quadrant elements (dropped where they lie in the
+// child's padding, as store_if does); phase 2: task (s, pos) combines the 7 children at
+// sub-quadrant s into the node's four quadrant elements.  Bit-identical to two launches.
+template <int L, int PT>
+__global__ void __launch_bounds__(4 * PT) postadd2_kernel(int algo, const uint32_t* __restrict__ grand, int64_t nodes,
+                                                         int rows, int cols, uint32_t* __restrict__ parent, int sh,
+                                                         uint32_t* err) {
+  constexpr int S = rec_stride(L);
+  extern __shared__ __align__(16) uint32_t s_v[];  // [c1][s][pos] records
+  const int hr1 = (rows + rows % 2) / 2, hc1 = (cols + cols % 2) / 2;
+  const int hr2 = (hr1 + hr1 % 2) / 2, hc2 = (hc1 + hc1 % 2) / 2;
+  const int64_t per2 = (int64_t)hr2 * hc2;
+  const int64_t tiles_per_node = (per2 + PT - 1) / PT;
+  const int64_t ntiles = tiles_per_node * nodes;
+  const int tid = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t node = tile / tiles_per_node;
+    const int64_t e0 = (tile - node * tiles_per_node) * PT;
+    uint32_t* P = parent + node * (int64_t)rows * cols * S;
+    for (int task = tid; task < 7 * PT; task += 4 * PT) {  // phase 1
+      const int c1 = task / PT, pos = task - c1 * PT;
+      const int64_t e = e0 + pos;
+      if (e >= per2) continue;
+      const int r2 = (int)(e / hc2), c2 = (int)(e - (int64_t)r2 * hc2);
+      const uint32_t* M = grand + (((node * 7 + c1) * 7) * per2 + e) * S;
+      auto ldc = [&](int k, MP<L>& x) { load_rec<L>(M + (int64_t)k * per2 * S, x); };
+      uint32_t* v = s_v + ((int64_t)c1 * 4 * PT + pos) * S;
+      auto put = [&](int q, const MP<L>& x) {
+        if (r2 + (q >> 1) * hr2 < hr1 && c2 + (q & 1) * hc2 < hc1) {
+          if (exp_out_of_range(x.e)) atomicOr(err, ERR_EXP_RANGE);
+          store_rec<L>(v + (int64_t)q * PT * S, x);
+        }
+      };
+      postadd_body<L>(algo, sh, ldc, put, [](const MP<L>&, const MP<L>&) {});
+    }
+    __syncthreads();
+    {  // phase 2: 4 PT tasks, one per thread
+      const int s = tid / PT, pos = tid - s * PT;
+      const int64_t e = e0 + pos;
+      if (e < per2) {
+        const int r2 = (int)(e / hc2), c2 = (int)(e - (int64_t)r2 * hc2);
+        const int r1 = r2 + (s >> 1) * hr2, c1 = c2 + (s & 1) * hc2;  // position inside the children
+        if (r1 < hr1 && c1 < hc1) {
+          const uint32_t* v = s_v + ((int64_t)s * PT + pos) * S;
+          auto ldc = [&](int k, MP<L>& x) { load_rec<L>(v + (int64_t)k * 4 * PT * S, x); };
+          auto put = [&](int q, const MP<L>& x) {
+            store_if<L>(P, rows, cols, r1 + (q >> 1) * hr1, c1 + (q & 1) * hc1, x, err);
+          };
+          postadd_body<L>(algo, sh, ldc, put, [](const MP<L>&, const MP<L>&) {});
+        }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -509,6 +653,30 @@ void launch_preadd_slots(int algo, int side, const uint32_t* parent, int rows, i
   const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2);
   preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, 1, rows, cols, children, sh, slots);
 }
+// two levels at once (preadd2_kernel): grand = 49 operands per node, each ceil(ceil(rows/2)/2) x
+// ceil(ceil(cols/2)/2); false when this limb count has no fused kernel (the caller runs two levels)
+template <int L>
+bool launch_preadd2(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
+                    uint32_t* grand, int sh, cudaStream_t st) {
+  if constexpr (L > 32 || L < 4) {
+    return false;
+  } else {
+    // measured (profiles/r02_ab_fuse2.jsonl, n = 1024 Winograd): 32 positions per CTA at 256 / 512
+    // bits (16: +1.5 %, 64: +3.5 / +12 %); 16 at 1024 bits (1.89 vs 2.10 ms: 129 KB of shared memory
+    // per CTA with 32)
+    constexpr int PT = L > 16 ? MPG_ADD2_PT / 2 : MPG_ADD2_PT;
+    constexpr int S = rec_stride(L);
+    const int hr1 = (rows + rows % 2) / 2, hc1 = (cols + cols % 2) / 2;
+    const int64_t per2 = (int64_t)((hr1 + hr1 % 2) / 2) * ((hc1 + hc1 % 2) / 2);
+    const int64_t ntiles = ((per2 + PT - 1) / PT) * nodes;
+    if (ntiles <= 0) return true;
+    const int smem = 7 * 4 * PT * S * (int)sizeof(uint32_t);
+    smem_attr_once((const void*)preadd2_kernel<L, PT>, smem);
+    const int grid = (int)std::min<int64_t>(ntiles, 148 * 64);
+    preadd2_kernel<L, PT><<<grid, 4 * PT, smem, st>>>(algo, side, parent, nodes, rows, cols, grand, sh);
+    return true;
+  }
+}
 template <int L>
 void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows, int cols,
                     uint32_t* parent, uint32_t* t_out, int sh, uint32_t* err, cudaStream_t st, const int* rowlist,
@@ -527,6 +695,27 @@ void launch_postadd(int algo, const uint32_t* children, int64_t nodes, int rows,
   if (total <= 0) return;
   postadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, children, nodes, rows, cols, parent, t_out, sh,
                                                      err, rowlist, nrows, cc0, ncc, rowtab);
+}
+// two levels at once (postadd2_kernel); false when this limb count has no fused kernel
+template <int L>
+bool launch_postadd2(int algo, const uint32_t* grand, int64_t nodes, int rows, int cols, uint32_t* parent,
+                     int sh, uint32_t* err, cudaStream_t st) {
+  // (at 1024 bits the fused combine needs 255 registers and runs 1.77 vs 1.07 ms: not offered)
+  if constexpr (!has_postadd2(L)) {
+    return false;
+  } else {
+    constexpr int PT = MPG_ADD2_PT;
+    constexpr int S = rec_stride(L);
+    const int hr1 = (rows + rows % 2) / 2, hc1 = (cols + cols % 2) / 2;
+    const int64_t per2 = (int64_t)((hr1 + hr1 % 2) / 2) * ((hc1 + hc1 % 2) / 2);
+    const int64_t ntiles = ((per2 + PT - 1) / PT) * nodes;
+    if (ntiles <= 0) return true;
+    const int smem = 7 * 4 * PT * S * (int)sizeof(uint32_t);
+    smem_attr_once((const void*)postadd2_kernel<L, PT>, smem);
+    const int grid = (int)std::min<int64_t>(ntiles, 148 * 64);
+    postadd2_kernel<L, PT><<<grid, 4 * PT, smem, st>>>(algo, grand, nodes, rows, cols, parent, sh, err);
+    return true;
+  }
 }
 template <int L>
 void launch_copy2d(const uint32_t* src, int64_t lds, uint32_t* dst, int64_t ldd, int rows, int cols,
@@ -558,7 +747,9 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t,   \
-                                int64_t);
+                                int64_t);                                                                \
+  template bool launch_preadd2<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int, cudaStream_t); \
+  template bool launch_postadd2<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, int, uint32_t*, cudaStream_t);
 #if MPG_WIDE
 #ifdef MPG_WIDE_L  // one wide limb count per translation unit (compile time)
 MPG_INST(MPG_WIDE_L)

@@ -88,6 +88,18 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
 template <int L>
 void launch_preadd_slots(int algo, int side, const uint32_t* parent, int rows, int cols, uint32_t* children,
                          ChildSlots slots, int sh, cudaStream_t st);
+// two levels of pre-additions in one launch (L <= 32): grand = the 49 grandchildren per node in the
+// layout two launch_preadd calls produce, the intermediate level kept in shared memory; returns
+// false when this limb count has no fused kernel
+template <int L>
+bool launch_preadd2(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
+                    uint32_t* grand, int sh, cudaStream_t st);
+// two levels of post-additions in one launch (L <= 32): the node's C from its 49 grandchildren
+// products (the layout two recursion levels produce); false when there is no fused kernel
+constexpr bool has_postadd2(int L) { return L >= 4 && L <= 16; }
+template <int L>
+bool launch_postadd2(int algo, const uint32_t* grand, int64_t nodes, int rows, int cols, uint32_t* parent,
+                     int sh, uint32_t* err, cudaStream_t st);
 // Children products (7 per parent, hm x hn) -> parent C (rows x cols, stripped).
 // Optional trace output of Winograd's T1/T2 (2 x hm x hn per parent) when t_out != nullptr.
 // rowlist (device, optional): only these child rows [0, hm) are combined (and the parent rows

@@ -229,7 +229,7 @@ std::vector<Level> plan_levels(int64_t m, int64_t l, int64_t n, int64_t n_min) {
 }
 
 // ---- recursion depth per precision from measured leaf throughput (north star (2)) ----
-// B200 measurements (tools/leaf_table.py -> profiles/r02_leaf_table_eo.jsonl, re-measured with the carry-chained product): Winograd products with
+// B200 measurements (tools/leaf_table.py -> profiles/r02_leaf_table_h.jsonl, re-measured with the carry-chained product and the fused two-level additions; the add rates are bytes of the one-launch-per-level model over the measured time): Winograd products with
 // 7^d leaves of s^3 (s = 16 .. 512) per limb count; the leaf kernel's MP multiply-adds per second and
 // the pre- / post-addition record bandwidth at that recursion level.  The leaf rate is flat for
 // s >= 32 and drops ~15 % at s = 16; the additions run at 2-4.5 TB/s.
@@ -242,14 +242,14 @@ struct LeafTab {
   double post[kTabSizes];  // post-add GB/s
 };
 constexpr LeafTab kLeafTab[] = {
-    {4, {1.286e11, 1.522e11, 1.496e11, 1.575e11, 1.576e11, 1.558e11}, {2180, 4261, 3841, 5167, 4859, 4259},
-     {2227, 4582, 4065, 5935, 5441, 4763}},
-    {8, {7.947e10, 9.115e10, 9.118e10, 9.462e10, 9.456e10, 9.441e10}, {2103, 3748, 3352, 4514, 4294, 3689},
-     {2230, 4380, 3903, 5518, 5135, 4459}},
-    {16, {3.653e10, 3.928e10, 3.894e10, 3.975e10, 3.969e10, 3.963e10}, {2259, 3496, 3174, 4071, 3814, 3465},
-     {2170, 3205, 2965, 3714, 3551, 3293}},
-    {32, {1.211e10, 1.271e10, 1.268e10, 1.289e10, 1.287e10, 1.286e10}, {1971, 3001, 2739, 3450, 3314, 3065},
-     {2277, 3491, 3161, 4060, 3840, 3482}},
+    {4, {1.393e11, 1.641e11, 1.614e11, 1.696e11, 1.689e11, 1.670e11}, {2974, 5778, 4445, 6385, 5959, 4318},
+     {2330, 4924, 3903, 5798, 5187, 4909}},
+    {8, {8.268e10, 9.487e10, 9.460e10, 9.782e10, 9.777e10, 9.765e10}, {2582, 5251, 4091, 5863, 5383, 4025},
+     {2117, 4402, 3618, 5761, 5187, 4581}},
+    {16, {3.663e10, 3.934e10, 3.904e10, 3.984e10, 3.977e10, 3.973e10}, {2958, 4880, 3882, 5241, 5179, 3499},
+     {2560, 3994, 3134, 4878, 4613, 3922}},
+    {32, {1.212e10, 1.270e10, 1.267e10, 1.287e10, 1.285e10, 1.284e10}, {2927, 4171, 3371, 4401, 4524, 3095},
+     {2352, 3580, 3198, 4174, 3947, 3547}},
 };
 
 // table row for L (L < 4: the 128-bit row; L > 32: the 1024-bit row with the rate scaled by (32/L)^2)

@@ -46,6 +46,9 @@ namespace mpg {
 #ifndef MPG_POST_MINB_32
 #define MPG_POST_MINB_32 1
 #endif
+#ifndef MPG_ADD2_STAGE
+#define MPG_ADD2_STAGE 1  // fused pre-additions: results stored through a per-warp staging row (whole sectors)
+#endif
 #ifndef MPG_ADD2_PT
 #define MPG_ADD2_PT 32  // positions per CTA of the fused two-level transforms (4 PT threads)
 #endif
@@ -311,8 +314,19 @@ __global__ void __launch_bounds__(4 * PT) preadd2_kernel(int algo, int side, con
         uint32_t* v = s_v + ((int64_t)s * PT + pos) * S;
         auto put = [&](int child, const MP<L>& x) { store_rec<L>(v + (int64_t)child * 4 * PT * S, x); };
         if (r1 < hr1 && c1 < hc1) {
+          // small records: the four quadrant elements loaded up front (independent loads in flight)
+          constexpr bool HOIST = MPG_ADDS_HOIST && L <= 8;
+          MP<L> Q[HOIST ? 4 : 1];
+          if constexpr (HOIST) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              load_padded<L>(P, rows, cols, r1 + (q >> 1) * hr1, c1 + (q & 1) * hc1, Q[q]);
+          }
           auto ld = [&](int q, MP<L>& x) {
-            load_padded<L>(P, rows, cols, r1 + (q >> 1) * hr1, c1 + (q & 1) * hc1, x);
+            if constexpr (HOIST)
+              x = Q[q];
+            else
+              load_padded<L>(P, rows, cols, r1 + (q >> 1) * hr1, c1 + (q & 1) * hc1, x);
           };
           preadd_body<L>(algo, side, sh, ld, put);
         } else {  // the children's own zero padding (odd child dimension)
@@ -324,7 +338,10 @@ __global__ void __launch_bounds__(4 * PT) preadd2_kernel(int algo, int side, con
       }
     }
     __syncthreads();
-    // phase 2: 7 PT tasks over 4 PT threads
+    // phase 2: 7 PT tasks over 4 PT threads.  A warp's 32 tasks share the child and cover 32
+    // consecutive positions, i.e. 32 consecutive records of every grandchild: when all 32 exist the
+    // warp passes each result through a staging row in shared memory and stores it as full,
+    // consecutive 16-byte chunks (whole sectors) instead of 16 bytes per lane at the record stride
     for (int task = tid; task < 7 * PT; task += 4 * PT) {
       const int c1 = task / PT, pos = task - c1 * PT;
       const int64_t e = e0 + pos;
@@ -332,7 +349,22 @@ __global__ void __launch_bounds__(4 * PT) preadd2_kernel(int algo, int side, con
       const uint32_t* v = s_v + ((int64_t)c1 * 4 * PT + pos) * S;
       auto ld = [&](int q, MP<L>& x) { load_rec<L>(v + (int64_t)q * PT * S, x); };
       uint32_t* out = grand + (((node * 7 + c1) * 7) * per2 + e) * S;
-      auto put = [&](int child, const MP<L>& x) { store_rec<L>(out + (int64_t)child * per2 * S, x); };
+      const int lane = tid & 31;
+      const bool warp_full = MPG_ADD2_STAGE && PT % 32 == 0 && (e - lane) + 32 <= per2;  // warp-uniform
+      uint32_t* stage = s_v + 7 * 4 * PT * S + (tid >> 5) * 32 * S;
+      auto put = [&](int child, const MP<L>& x) {
+        if (warp_full) {
+          store_rec<L>(stage + lane * S, x);
+          __syncwarp();
+          uint4* dst = reinterpret_cast<uint4*>(out - lane * S + (int64_t)child * per2 * S);
+          const uint4* src = reinterpret_cast<const uint4*>(stage);
+#pragma unroll
+          for (int q = 0; q < S / 4; ++q) dst[lane + 32 * q] = src[lane + 32 * q];
+          __syncwarp();
+        } else {
+          store_rec<L>(out + (int64_t)child * per2 * S, x);
+        }
+      };
       preadd_body<L>(algo, side, sh, ld, put);
     }
     __syncthreads();
@@ -529,7 +561,18 @@ __global__ void __launch_bounds__(4 * PT) postadd2_kernel(int algo, const uint32
       if (e >= per2) continue;
       const int r2 = (int)(e / hc2), c2 = (int)(e - (int64_t)r2 * hc2);
       const uint32_t* M = grand + (((node * 7 + c1) * 7) * per2 + e) * S;
-      auto ldc = [&](int k, MP<L>& x) { load_rec<L>(M + (int64_t)k * per2 * S, x); };
+      constexpr bool HOIST = MPG_ADDS_HOIST && L <= 8;  // the seven products loaded up front
+      MP<L> Mv[HOIST ? 7 : 1];
+      if constexpr (HOIST) {
+#pragma unroll
+        for (int k = 0; k < 7; ++k) load_rec<L>(M + (int64_t)k * per2 * S, Mv[k]);
+      }
+      auto ldc = [&](int k, MP<L>& x) {
+        if constexpr (HOIST)
+          x = Mv[k];
+        else
+          load_rec<L>(M + (int64_t)k * per2 * S, x);
+      };
       uint32_t* v = s_v + ((int64_t)c1 * 4 * PT + pos) * S;
       auto put = [&](int q, const MP<L>& x) {
         if (r2 + (q >> 1) * hr2 < hr1 && c2 + (q & 1) * hc2 < hc1) {
@@ -670,7 +713,7 @@ bool launch_preadd2(int algo, int side, const uint32_t* parent, int64_t nodes, i
     const int64_t per2 = (int64_t)((hr1 + hr1 % 2) / 2) * ((hc1 + hc1 % 2) / 2);
     const int64_t ntiles = ((per2 + PT - 1) / PT) * nodes;
     if (ntiles <= 0) return true;
-    const int smem = 7 * 4 * PT * S * (int)sizeof(uint32_t);
+    const int smem = (7 * 4 * PT + 4 * PT) * S * (int)sizeof(uint32_t);  // children + one staging row per warp
     smem_attr_once((const void*)preadd2_kernel<L, PT>, smem);
     const int grid = (int)std::min<int64_t>(ntiles, 148 * 64);
     preadd2_kernel<L, PT><<<grid, 4 * PT, smem, st>>>(algo, side, parent, nodes, rows, cols, grand, sh);

@@ -246,6 +246,7 @@ template <int L>
 __global__ void __launch_bounds__(256, pre_minb(L)) preadd_kernel(int algo, int side, const uint32_t* __restrict__ parent, int64_t nodes,
                               int rows, int cols, uint32_t* __restrict__ children, int sh, ChildSlots slots) {
   constexpr int S = rec_stride(L);
+  extern __shared__ __align__(16) uint32_t s_stage[];  // one staging row of 32 records per warp
   const int hr = (rows + rows % 2) / 2, hc = (cols + cols % 2) / 2;
   const int64_t per = (int64_t)hr * hc;
   const int64_t total = per * nodes;
@@ -271,10 +272,29 @@ __global__ void __launch_bounds__(256, pre_minb(L)) preadd_kernel(int algo, int 
       else
         load_padded<L>(P, rows, cols, r + (q >> 1) * hr, c + (q & 1) * hc, x);
     };
+    // a warp's 32 elements are 32 consecutive records of every child when they all exist and
+    // belong to one node: then each result goes through the warp's staging row in shared memory
+    // and is stored as whole consecutive 16-byte chunks (full sectors) instead of 16 bytes per
+    // lane at the record stride (measured on the fused kernel: -18 % pre-addition time)
+    const int lane = threadIdx.x & 31;
+    const int64_t t0 = t - lane;
+    const bool warp_full = MPG_ADD2_STAGE && L <= 32 && t0 + 32 <= total && t0 / per == (t0 + 31) / per;  // warp-uniform
+    uint32_t* stage = s_stage + (threadIdx.x >> 5) * 32 * S;
     // slots.s[child]: output slot of each child, < 0: not produced (the pipelined host GEMM
     // forms its top-level children in two steps); the identity map otherwise
     auto put = [&](int child, const MP<L>& x) {
-      if (slots.s[child] >= 0) store_rec<L>(out + slots.s[child] * cs, x);
+      if (slots.s[child] < 0) return;
+      if (warp_full) {
+        store_rec<L>(stage + lane * S, x);
+        __syncwarp();
+        uint4* dst = reinterpret_cast<uint4*>(out - lane * S + slots.s[child] * cs);
+        const uint4* src = reinterpret_cast<const uint4*>(stage);
+#pragma unroll
+        for (int q = 0; q < S / 4; ++q) dst[lane + 32 * q] = src[lane + 32 * q];
+        __syncwarp();
+      } else {
+        store_rec<L>(out + slots.s[child] * cs, x);
+      }
     };
     preadd_body<L>(algo, side, sh, ld, put);
   }
@@ -679,6 +699,13 @@ void launch_vec_op(int op, const uint32_t* A, const uint32_t* B, uint32_t* C, in
   vec_op_kernel<L><<<grid_for(N), NT, 0, st>>>(op, A, B, C, N, sh, err);
 }
 template <int L>
+int preadd_stage_bytes() {  // preadd_kernel's staging rows (one per warp; register-resident formats only)
+  if (!MPG_ADD2_STAGE || L > 32) return 0;
+  const int bytes = (NT / 32) * 32 * rec_stride(L) * (int)sizeof(uint32_t);
+  smem_attr_once((const void*)preadd_kernel<L>, bytes);
+  return bytes;
+}
+template <int L>
 void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, int rows, int cols,
                    uint32_t* children, int sh, uint32_t* err, cudaStream_t st) {
   (void)err;
@@ -687,14 +714,16 @@ void launch_preadd(int algo, int side, const uint32_t* parent, int64_t nodes, in
     if (wmp::enabled()) return wmp::launch_preadd<L / 32>(algo, side, parent, nodes, rows, cols, children, sh, st);
 #endif
   const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2) * nodes;
-  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, nodes, rows, cols, children, sh,
-                                                    ChildSlots{{0, 1, 2, 3, 4, 5, 6}});
+  preadd_kernel<L><<<grid_for(total), NT, preadd_stage_bytes<L>(), st>>>(algo, side, parent, nodes, rows, cols,
+                                                                          children, sh,
+                                                                          ChildSlots{{0, 1, 2, 3, 4, 5, 6}});
 }
 template <int L>
 void launch_preadd_slots(int algo, int side, const uint32_t* parent, int rows, int cols, uint32_t* children,
                          ChildSlots slots, int sh, cudaStream_t st) {
   const int64_t total = (int64_t)((rows + rows % 2) / 2) * ((cols + cols % 2) / 2);
-  preadd_kernel<L><<<grid_for(total), NT, 0, st>>>(algo, side, parent, 1, rows, cols, children, sh, slots);
+  preadd_kernel<L><<<grid_for(total), NT, preadd_stage_bytes<L>(), st>>>(algo, side, parent, 1, rows, cols, children,
+                                                                          sh, slots);
 }
 // two levels at once (preadd2_kernel): grand = 49 operands per node, each ceil(ceil(rows/2)/2) x
 // ceil(ceil(cols/2)/2); false when this limb count has no fused kernel (the caller runs two levels)

@@ -19,7 +19,8 @@ BUILD = PKG / "_build"
 LIB = PKG / "libmpgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "lu.cu", "capi.cu", "group.cu",
+SOURCES = ["gemm.cu", "gemm_tc.cu", "metrics.cu", "elementwise.cu", "elementwise_fused8.cu",
+           "elementwise_fused16.cu", "elementwise_fused32.cu", "lu.cu", "capi.cu", "group.cu",
            "gemm_wide.cu", "metrics_wide.cu"] + \
     [f"{k}_wide{L}.cu" for k in ("elementwise", "lu") for L in (64, 128, 256, 288)]
 HEADERS = ["mp_arith.cuh", "kernels.h", "wmp.cuh", "wkern.cuh"]
@@ -36,7 +37,7 @@ def _newest_dep() -> float:
 def _compile(src: str, force: bool) -> Path:
     obj = BUILD / (src + ".o")
     s = CSRC / src
-    srcs = [s] + ([CSRC / re.sub(r"_wide\d*", "", src)] if "_wide" in src else [])  # *_wide*.cu include *.cu
+    srcs = [s] + ([CSRC / re.sub(r"_(wide|fused)\d*", "", src)] if ("_wide" in src or "_fused" in src) else [])  # *_wide*.cu / *_fused*.cu include *.cu
     if (not force and obj.exists() and all(obj.stat().st_mtime >= x.stat().st_mtime for x in srcs)
             and obj.stat().st_mtime >= _newest_dep()):
         return obj

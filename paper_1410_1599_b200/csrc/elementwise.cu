@@ -801,6 +801,21 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   convert_kernel<L><<<grid_for(N), NT, 0, st>>>(src, ls, rec_stride(ls), N, dst, sh, err);
 }
 
+// the fused two-level transforms are instantiated in their own translation units
+// (elementwise_fused{8,16,32}.cu: MPG_EW_PART = 1, 2, 3), which compile beside this one
+#define MPG_INST_FUSED(L)                                                                                       \
+  template bool launch_preadd2<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int, cudaStream_t); \
+  template bool launch_postadd2<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, int, uint32_t*, cudaStream_t);
+#if MPG_EW_PART == 1
+MPG_INST_FUSED(1)
+MPG_INST_FUSED(2)
+MPG_INST_FUSED(4)
+MPG_INST_FUSED(8)
+#elif MPG_EW_PART == 2
+MPG_INST_FUSED(16)
+#elif MPG_EW_PART == 3
+MPG_INST_FUSED(32)
+#else
 #define MPG_INST(L)                                                                                     \
   template void launch_soa2rec<L>(const uint32_t*, const int32_t*, const uint8_t*, int64_t, int64_t,   \
                                   uint32_t*, cudaStream_t);                                             \
@@ -819,17 +834,20 @@ void launch_convert(const uint32_t* src, int ls, int64_t N, uint32_t* dst, int s
   template void launch_copy2d<L>(const uint32_t*, int64_t, uint32_t*, int64_t, int, int, cudaStream_t); \
   template void launch_convert<L>(const uint32_t*, int, int64_t, uint32_t*, int, uint32_t*, cudaStream_t); \
   template void launch_sub2d<L>(uint32_t*, int64_t, const uint32_t*, int, int, int, uint32_t*, cudaStream_t,   \
-                                int64_t);                                                                \
-  template bool launch_preadd2<L>(int, int, const uint32_t*, int64_t, int, int, uint32_t*, int, cudaStream_t); \
-  template bool launch_postadd2<L>(int, const uint32_t*, int64_t, int, int, uint32_t*, int, uint32_t*, cudaStream_t);
+                                int64_t);
 #if MPG_WIDE
 #ifdef MPG_WIDE_L  // one wide limb count per translation unit (compile time)
 MPG_INST(MPG_WIDE_L)
+MPG_INST_FUSED(MPG_WIDE_L)
 #else
 MPG_INST(64)
 MPG_INST(128)
 MPG_INST(256)
 MPG_INST(288)
+MPG_INST_FUSED(64)
+MPG_INST_FUSED(128)
+MPG_INST_FUSED(256)
+MPG_INST_FUSED(288)
 #endif
 #else
 MPG_INST(1)
@@ -848,5 +866,6 @@ MPG_INST_SLOTS(8)
 MPG_INST_SLOTS(16)
 MPG_INST_SLOTS(32)
 #endif
+#endif  // MPG_EW_PART
 
 }  // namespace mpg

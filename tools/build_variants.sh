@@ -9,7 +9,7 @@ NVCC="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -line
 while [ $# -gt 0 ]; do
   name=$1; flags=$2; shift 2
   d=$OUT/$name; mkdir -p $d
-  ALL="gemm gemm_tc metrics elementwise lu capi group gemm_wide metrics_wide elementwise_wide64 elementwise_wide128 elementwise_wide256 elementwise_wide288 lu_wide64 lu_wide128 lu_wide256 lu_wide288"
+  ALL="gemm gemm_tc metrics elementwise elementwise_fused8 elementwise_fused16 elementwise_fused32 lu capi group gemm_wide metrics_wide elementwise_wide64 elementwise_wide128 elementwise_wide256 elementwise_wide288 lu_wide64 lu_wide128 lu_wide256 lu_wide288"
   for s in $ALL; do
     if [ -n "$ONLY" ] && ! [[ " $ONLY " == *" $s "* ]]; then
       cp paper_1410_1599_b200/_build/$s.cu.o $d/$s.o  # ONLY="gemm ...": reuse the main build's other objects

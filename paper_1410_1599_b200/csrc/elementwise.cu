@@ -49,6 +49,9 @@ namespace mpg {
 #ifndef MPG_ADD2_STAGE
 #define MPG_ADD2_STAGE 1  // fused pre-additions: results stored through a per-warp staging row (whole sectors)
 #endif
+#ifndef MPG_POST2_MINB
+#define MPG_POST2_MINB 1  // resident CTAs asked for the fused post-additions; measured: 5 / 6 CTAs (102 / 85 registers, spilling) 0.25 -> 0.32 / 0.35 ms at cfg2
+#endif
 #ifndef MPG_ADD2_PT
 #define MPG_ADD2_PT 32  // positions per CTA of the fused two-level transforms (4 PT threads)
 #endif
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(256, post_minb(L)) postadd_kernel(int algo, co
 // child's padding, as store_if does); phase 2: task (s, pos) combines the 7 children at
 // sub-quadrant s into the node's four quadrant elements.  Bit-identical to two launches.
 template <int L, int PT>
-__global__ void __launch_bounds__(4 * PT) postadd2_kernel(int algo, const uint32_t* __restrict__ grand, int64_t nodes,
+__global__ void __launch_bounds__(4 * PT, MPG_POST2_MINB) postadd2_kernel(int algo, const uint32_t* __restrict__ grand, int64_t nodes,
                                                          int rows, int cols, uint32_t* __restrict__ parent, int sh,
                                                          uint32_t* err) {
   constexpr int S = rec_stride(L);

@@ -25,7 +25,7 @@
 #endif
 
 #ifndef MPG_MINB_8
-#define MPG_MINB_8 8  // with 8 x 16 tiles and k-tile 12: 8 CTAs of 128 threads per SM (measured: -1.1 % at cfg2, -3.8 % on the cfg3 shape vs 4 x 256, 16 x 16, k-tile 16)
+#define MPG_MINB_8 6  // 8 x 16 tiles of 128 threads; with k-tile 16 shared memory holds 6 CTAs per SM, so the register cap is 80 (70 used): -0.3 % vs a cap of 64 (profiles/r02_ab_tk.jsonl)
 #endif
 #define MPG_MINB_1 4
 #define MPG_MINB_2 4
@@ -137,7 +137,7 @@ __device__ __forceinline__ void lds_rec(uint32_t addr, MP<L>& x) {
 #endif
 
 #ifndef MPG_TK_8
-#define MPG_TK_8 12
+#define MPG_TK_8 16  // 16 (6 CTAs per SM by shared memory, whole k-tiles at l = 32 / 64) vs 12 (8 CTAs): leaf -0.3 % at l = 64, -0.9 % at l = 32, LU -0.5 % (profiles/r02_ab_tk.jsonl)
 #endif
 
 #ifndef MPG_U_8
